@@ -1,0 +1,202 @@
+/* ozgpu.h -- C-ABI of the B200-native Ozaki-I FP64 GEMM (integer-slice
+ * emulation, arXiv 2506.11277).  This is the drop-in boundary for the
+ * reference library's GEMM path (ozmul, /root/reference/proj): every entry
+ * point cites the reference interface it replaces.  Plain pointers and
+ * sizes only; no C++ or torch types cross this boundary.
+ *
+ * Error codes (the reference's exception classes, scheme.cpp:221-239,
+ * main.cpp:770-783):
+ *   OZGPU_OK 0, OZGPU_INVALID_ARGUMENT 1 (std::invalid_argument),
+ *   OZGPU_DOMAIN_ERROR 2 (std::domain_error), OZGPU_DEVICE_ERROR 3,
+ *   OZGPU_INFEASIBLE 4 (SelectionInfeasible), OZGPU_OVERFLOW 5
+ *   (MmaOverflowError).  ozgpu_last_error() returns the calling thread's
+ *   message for the last failing call, worded like the reference's.
+ *
+ * Enumerations match the reference headers:
+ *   schedule: 0 kFull, 1 kReduced                       (scheme.hpp:30-33)
+ *   strategy: 0 kFloatPerProduct, 1 kDiagonalInteger, 2 kLevelledExact
+ *                                                        (scheme.hpp:45-49)
+ *   mode:     0 kTruncate, 1 kNearest                    (slicing.hpp SliceMode)
+ *   orientation: 0 rows (left factor), 1 columns (right factor)
+ *
+ * Threading: every call is safe from any number of host threads
+ * (SPEC.md:91,363-364); calls on one context serialise on its stream.
+ */
+#ifndef OZGPU_H
+#define OZGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OZGPU_OK 0
+#define OZGPU_INVALID_ARGUMENT 1
+#define OZGPU_DOMAIN_ERROR 2
+#define OZGPU_DEVICE_ERROR 3
+#define OZGPU_INFEASIBLE 4
+#define OZGPU_OVERFLOW 5
+
+#define OZGPU_MAX_LEVELS 128
+
+/* MmaConfig (proj/include/ozmul/mma_sim.hpp:27-37): inputs in I_{t'},
+ * accumulation in I_T.  int8_int32 = {7, 31}. */
+typedef struct {
+  int input_width; /* t' */
+  int acc_width;   /* T  */
+} ozgpu_mma_config;
+
+/* MultiplyPlan (proj/include/ozmul/scheme.hpp:77-88) incl. Schedule and
+ * LevelPlan (scheme.hpp:36-56). */
+typedef struct {
+  int slices_a;
+  int slices_b;
+  int width;          /* t */
+  int schedule;       /* 0 full, 1 reduced */
+  int diag_sum_limit; /* Schedule::diag_sum_limit; <= 0 means unset */
+  int strategy;       /* 0 float-per-product, 1 diagonal-integer, 2 levelled-exact */
+  int mode;           /* 0 truncate, 1 nearest */
+  int precision;      /* p */
+  int acc_bits_used;  /* T' = 2t + ceil(log2 k) */
+  int num_levels;
+  int levels[2 * OZGPU_MAX_LEVELS]; /* inclusive [first, last] diagonal pairs */
+  long long level_inexact_adds;     /* LevelPlan::inexact_adds */
+  long long psi;
+} ozgpu_plan;
+
+/* Diagnostics (proj/include/ozmul/scheme.hpp:97-106). */
+typedef struct {
+  int64_t products;
+  int64_t integer_adds;
+  int64_t float_adds;
+  int64_t flushes;
+  long long realized_psi;
+  long long planned_psi;
+  int width;
+  int acc_bits_used;
+} ozgpu_diag;
+
+/* SliceSelection (proj/include/ozmul/analysis.hpp:86-92) and the
+ * SelectionInfeasible payload (analysis.hpp:78-84). */
+typedef struct {
+  int slices_a;
+  int slices_b;
+  double lhs;
+  double target;
+  int64_t products;
+  double gap; /* set when OZGPU_INFEASIBLE */
+} ozgpu_selection;
+
+/* ScalingProfile's scalar part (proj/include/ozmul/analysis.hpp:30-38). */
+typedef struct {
+  double kappa_a;
+  double kappa_b;
+  int a_has_zero_block;
+  int b_has_zero_block;
+} ozgpu_profile;
+
+typedef struct ozgpu_ctx ozgpu_ctx;
+
+/* ---- library / context ------------------------------------------------ */
+const char* ozgpu_last_error(void);
+const char* ozgpu_version(void);
+/* Creates a context on CUDA device `device` (own stream + workspace).
+ * Fails with OZGPU_DEVICE_ERROR when no sm_100 device is present: there is
+ * no CPU fallback. */
+int ozgpu_create(int device, ozgpu_ctx** out);
+int ozgpu_destroy(ozgpu_ctx* ctx);
+/* Number of this library's kernels launched through `ctx` so far. */
+int64_t ozgpu_kernel_launches(const ozgpu_ctx* ctx);
+/* The process-wide default context for `device` (created on first use). */
+ozgpu_ctx* ozgpu_default_context(int device);
+/* Per-stage device timing of the multiplies issued through `ctx` while
+ * enabled: CUDA events recorded on the launching stream around the slicing
+ * kernels, the tcgen05 pair-GEMM kernel and the combine kernel. */
+int ozgpu_set_stage_timing(ozgpu_ctx* ctx, int enable);
+/* Accumulated stage times since the last reset (synchronises the pending
+ * events): ms3[0] slicing, ms3[1] pair GEMMs, ms3[2] combine; *calls =
+ * number of timed multiplies. */
+int ozgpu_stage_times(ozgpu_ctx* ctx, double* ms3, int64_t* calls, int reset);
+
+/* ---- plan (host; O(s^2) scalar code) ---------------------------------- */
+/* optimal_slice_width, proj/src/mma_sim.cpp:50-59 */
+int ozgpu_optimal_slice_width(ozgpu_mma_config cfg, int64_t k, int* out);
+/* max_inner_dim, proj/src/mma_sim.cpp:66-72 */
+int ozgpu_max_inner_dim(ozgpu_mma_config cfg, int64_t* out);
+/* chi, proj/src/scheme.cpp:46-52 */
+int ozgpu_chi(int slices_a, int slices_b, int64_t* out);
+/* spare_carries, proj/src/scheme.cpp:54-62 */
+int ozgpu_spare_carries(int first_diag, int last_diag, int width, int64_t* out);
+/* plan_levels, proj/src/scheme.cpp:64-95 (levels written into plan->levels) */
+int ozgpu_plan_levels(int precision, int width, int acc_bits_used, int num_diagonals,
+                      ozgpu_plan* out);
+/* diagonal_flush_threshold, proj/src/scheme.cpp:97-106 */
+int ozgpu_diagonal_flush_threshold(ozgpu_mma_config cfg, int width, int64_t k, int64_t* out);
+/* make_plan, proj/src/scheme.cpp:127-168 */
+int ozgpu_make_plan(ozgpu_mma_config cfg, int64_t k, int slices_a, int slices_b,
+                    int schedule, int strategy, int mode, int precision, ozgpu_plan* out);
+
+/* ---- estimator -------------------------------------------------------- */
+/* select_slices, proj/src/analysis.cpp:142-207.  has_target=0 -> the
+ * default target gamma_psi of each candidate's plan. */
+int ozgpu_select_slices(double kappa_a, double kappa_b, int width, double u, int s_max,
+                        int has_target, double target, int schedule, int strategy,
+                        int acc_bits_used, int precision, ozgpu_selection* out);
+/* scaling_profile, proj/src/analysis.cpp:58-68, computed on the GPU.
+ * Host pointers; A m x k (lda), B k x n (ldb), row-major. */
+int ozgpu_scaling_profile(ozgpu_ctx* ctx, int64_t m, int64_t k, int64_t n, const double* a,
+                          int64_t lda, const double* b, int64_t ldb, ozgpu_profile* out);
+
+/* ---- the GEMM (multiply, proj/src/scheme.cpp:219-361) ------------------ */
+/* Host buffers: A m x k (lda), B k x n (ldb), C m x n (ldc), all row-major
+ * binary64.  Copies in, runs slicing + int8 tcgen05 pair GEMMs + exact
+ * epilogue on the GPU, copies C out.  diag may be NULL. */
+int ozgpu_dgemm(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda,
+                const double* b, int64_t ldb, double* c, int64_t ldc, ozgpu_mma_config cfg,
+                const ozgpu_plan* plan, ozgpu_diag* diag);
+/* multiply_axpby, proj/src/scheme.cpp:363-372: D = alpha*(AB) + beta*C in
+ * plain binary64 after the emulated product.  C is read from c_in (ldc),
+ * D written to d_out (ldd); they may alias. */
+int ozgpu_dgemm_axpby(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha,
+                      const double* a, int64_t lda, const double* b, int64_t ldb, double beta,
+                      const double* c_in, int64_t ldc, double* d_out, int64_t ldd,
+                      ozgpu_mma_config cfg, const ozgpu_plan* plan, ozgpu_diag* diag);
+/* Device-resident twin: a, b, c are device pointers; the work is enqueued on
+ * `stream` (0 = the context stream) and the call returns without
+ * synchronising.  Input validity (Inf/NaN/-0, scheme.cpp:223-225) is
+ * reported through *dev_status (device int, may be NULL): 0 ok, 1 dirty. */
+int ozgpu_dgemm_device(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a,
+                       int64_t lda, const double* b, int64_t ldb, double* c, int64_t ldc,
+                       ozgpu_mma_config cfg, const ozgpu_plan* plan, void* stream,
+                       int* dev_status, ozgpu_diag* diag);
+
+/* ---- debug hooks (bit-exact against the reference) --------------------- */
+/* split_rows / split_cols, proj/src/slicing.cpp:67-132, on the GPU.
+ * slices_out: [count][rows][cols] int64 (the reference's IntMatrix layout);
+ * scales_out: rows (orientation 0) or cols (orientation 1) ints. */
+int ozgpu_split(ozgpu_ctx* ctx, int orientation, int64_t rows, int64_t cols, const double* x,
+                int64_t ldx, int width, int count, int mode, int64_t* slices_out,
+                int* scales_out);
+/* integer_gemm, proj/src/mma_sim.cpp:76-125: exact X (m x k) * Y (k x n)
+ * on the tcgen05 int8 path (int32 accumulation in TMEM); when the inputs
+ * do not fit int8 or the bound k*max|x|*max|y| can exceed I_T, an exact
+ * CUDA-core path with per-MAC overflow checking (mma_sim.cpp:103-112) runs
+ * instead.  c may be NULL (no accumulator input). */
+int ozgpu_integer_gemm(ozgpu_ctx* ctx, int64_t m, int64_t k, int64_t n, const int64_t* x,
+                       const int64_t* y, const int64_t* c, int64_t* out, ozgpu_mma_config cfg);
+
+/* ---- synthetic inputs (proj/src/generators.cpp:25-49,176-182) ---------- */
+/* random_uniform: mt19937_64 seeded through splitmix64, identical bytes to
+ * the reference generator.  Host buffer, m x n row-major. */
+void ozgpu_random_uniform(int64_t m, int64_t n, uint64_t seed, double lo, double hi,
+                          double* out);
+/* gen_kappa_d, proj/src/generators.cpp:103-140 */
+void ozgpu_gen_kappa_d(int64_t n, double kappa_d, uint64_t seed, int rotate, double* a_out,
+                       double* b_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OZGPU_H */

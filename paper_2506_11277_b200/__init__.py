@@ -1,0 +1,597 @@
+"""B200-native Ozaki-I FP64 GEMM (integer-slice emulation, arXiv 2506.11277).
+
+Python mirror of the reference library's GEMM-path API (``ozmul``,
+/root/reference/proj/include/ozmul/{scheme,analysis,slicing,mma_sim}.hpp)
+over the C-ABI in ``include/ozgpu.h`` (``lib/libozgpu.so``).  Same names,
+argument meanings and error classes as the reference:
+
+    make_plan(cfg, k, slices_a, slices_b, schedule, strategy, mode, precision)
+    multiply(a, b, cfg, plan) -> MultiplyResult(c, diagnostics)
+    multiply_axpby(alpha, a, b, beta, c, cfg, plan)
+    select_slices(kappa_a, kappa_b, width, u, s_max, options)
+    scaling_profile(a, b)
+    split_rows / split_cols / integer_gemm          (bit-exact debug hooks)
+    chi / plan_levels / spare_carries / diagonal_flush_threshold /
+    optimal_slice_width / max_inner_dim
+
+All compute runs on the GPU through the native library; there is no CPU
+fallback.  Importing the package fails loudly when the library is missing.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+import os
+import threading
+from dataclasses import dataclass, field
+from typing import List, Optional, Tuple
+
+import numpy as np
+
+__all__ = [
+    "ScheduleKind", "Accumulation", "SliceMode", "BlockOrientation", "MmaConfig",
+    "MultiplyPlan", "Diagnostics", "MultiplyResult", "SliceSelection", "SelectOptions",
+    "ScalingProfile", "SlicedMatrix", "OzmulError", "InvalidArgument", "DomainError",
+    "DeviceError", "SelectionInfeasible", "MmaOverflowError", "make_plan", "multiply",
+    "multiply_axpby", "multiply_device", "select_slices", "scaling_profile", "split_rows",
+    "split_cols", "integer_gemm", "chi", "plan_levels", "spare_carries",
+    "diagonal_flush_threshold", "optimal_slice_width", "max_inner_dim", "random_uniform",
+    "gen_kappa_d", "kernel_launches", "library_path",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "lib", "libozgpu.so")
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+if not os.path.exists(_LIB_PATH):
+    raise ImportError(
+        f"{_LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(the Ozaki-I path has no CPU fallback)")
+
+_lib = ctypes.CDLL(_LIB_PATH)
+
+# --------------------------------------------------------------------- ABI
+
+
+class _Cfg(ctypes.Structure):
+    _fields_ = [("input_width", ctypes.c_int), ("acc_width", ctypes.c_int)]
+
+
+_MAX_LEVELS = 128
+
+
+class _Plan(ctypes.Structure):
+    _fields_ = [
+        ("slices_a", ctypes.c_int), ("slices_b", ctypes.c_int), ("width", ctypes.c_int),
+        ("schedule", ctypes.c_int), ("diag_sum_limit", ctypes.c_int),
+        ("strategy", ctypes.c_int), ("mode", ctypes.c_int), ("precision", ctypes.c_int),
+        ("acc_bits_used", ctypes.c_int), ("num_levels", ctypes.c_int),
+        ("levels", ctypes.c_int * (2 * _MAX_LEVELS)), ("level_inexact_adds", ctypes.c_longlong),
+        ("psi", ctypes.c_longlong),
+    ]
+
+
+class _Diag(ctypes.Structure):
+    _fields_ = [
+        ("products", ctypes.c_int64), ("integer_adds", ctypes.c_int64),
+        ("float_adds", ctypes.c_int64), ("flushes", ctypes.c_int64),
+        ("realized_psi", ctypes.c_longlong), ("planned_psi", ctypes.c_longlong),
+        ("width", ctypes.c_int), ("acc_bits_used", ctypes.c_int),
+    ]
+
+
+class _Sel(ctypes.Structure):
+    _fields_ = [("slices_a", ctypes.c_int), ("slices_b", ctypes.c_int), ("lhs", ctypes.c_double),
+                ("target", ctypes.c_double), ("products", ctypes.c_int64),
+                ("gap", ctypes.c_double)]
+
+
+class _Prof(ctypes.Structure):
+    _fields_ = [("kappa_a", ctypes.c_double), ("kappa_b", ctypes.c_double),
+                ("a_has_zero_block", ctypes.c_int), ("b_has_zero_block", ctypes.c_int)]
+
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_DP = ctypes.POINTER(ctypes.c_double)
+
+
+def _sig(name, restype, *argtypes):
+    f = getattr(_lib, name)
+    f.restype = restype
+    f.argtypes = list(argtypes)
+    return f
+
+
+_sig("ozgpu_last_error", ctypes.c_char_p)
+_sig("ozgpu_version", ctypes.c_char_p)
+_sig("ozgpu_create", ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P))
+_sig("ozgpu_destroy", ctypes.c_int, _P)
+_sig("ozgpu_kernel_launches", _I64, _P)
+_sig("ozgpu_default_context", _P, ctypes.c_int)
+_sig("ozgpu_optimal_slice_width", ctypes.c_int, _Cfg, _I64, ctypes.POINTER(ctypes.c_int))
+_sig("ozgpu_max_inner_dim", ctypes.c_int, _Cfg, ctypes.POINTER(_I64))
+_sig("ozgpu_chi", ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_I64))
+_sig("ozgpu_spare_carries", ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+     ctypes.POINTER(_I64))
+_sig("ozgpu_plan_levels", ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+     ctypes.POINTER(_Plan))
+_sig("ozgpu_diagonal_flush_threshold", ctypes.c_int, _Cfg, ctypes.c_int, _I64,
+     ctypes.POINTER(_I64))
+_sig("ozgpu_make_plan", ctypes.c_int, _Cfg, _I64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+     ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_Plan))
+_sig("ozgpu_select_slices", ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+     ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int,
+     ctypes.c_int, ctypes.c_int, ctypes.POINTER(_Sel))
+_sig("ozgpu_scaling_profile", ctypes.c_int, _P, _I64, _I64, _I64, _DP, _I64, _DP, _I64,
+     ctypes.POINTER(_Prof))
+_sig("ozgpu_dgemm", ctypes.c_int, _P, _I64, _I64, _I64, _DP, _I64, _DP, _I64, _DP, _I64, _Cfg,
+     ctypes.POINTER(_Plan), ctypes.POINTER(_Diag))
+_sig("ozgpu_dgemm_axpby", ctypes.c_int, _P, _I64, _I64, _I64, ctypes.c_double, _DP, _I64, _DP,
+     _I64, ctypes.c_double, _DP, _I64, _DP, _I64, _Cfg, ctypes.POINTER(_Plan),
+     ctypes.POINTER(_Diag))
+_sig("ozgpu_dgemm_device", ctypes.c_int, _P, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64, _Cfg,
+     ctypes.POINTER(_Plan), _P, _P, ctypes.POINTER(_Diag))
+_sig("ozgpu_split", ctypes.c_int, _P, ctypes.c_int, _I64, _I64, _DP, _I64, ctypes.c_int,
+     ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int))
+_sig("ozgpu_integer_gemm", ctypes.c_int, _P, _I64, _I64, _I64, ctypes.POINTER(ctypes.c_int64),
+     ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
+     ctypes.POINTER(ctypes.c_int64), _Cfg)
+_sig("ozgpu_random_uniform", None, _I64, _I64, ctypes.c_uint64, ctypes.c_double, ctypes.c_double,
+     _DP)
+_sig("ozgpu_gen_kappa_d", None, _I64, ctypes.c_double, ctypes.c_uint64, ctypes.c_int, _DP, _DP)
+
+# ------------------------------------------------------------------ errors
+
+
+class OzmulError(Exception):
+    """Base class; ``code`` is the C-ABI error code."""
+    code = 3
+
+
+class InvalidArgument(OzmulError, ValueError):
+    """std::invalid_argument in the reference."""
+    code = 1
+
+
+class DomainError(OzmulError, ArithmeticError):
+    """std::domain_error in the reference (capacity / precision)."""
+    code = 2
+
+
+class DeviceError(OzmulError, RuntimeError):
+    """CUDA failure or no sm_100 device (there is no CPU fallback)."""
+    code = 3
+
+
+class SelectionInfeasible(OzmulError, RuntimeError):
+    """analysis.hpp:78-84: no (s_A, s_B) meets the target."""
+    code = 4
+
+    def __init__(self, msg, gap=0.0, best_lhs=0.0, target=0.0):
+        super().__init__(msg)
+        self.gap, self.best_lhs, self.target = gap, best_lhs, target
+
+
+class MmaOverflowError(OzmulError, RuntimeError):
+    """mma_sim.hpp:41-46: a simulated accumulator left I_T."""
+    code = 5
+
+
+_ERRORS = {1: InvalidArgument, 2: DomainError, 3: DeviceError, 4: SelectionInfeasible,
+           5: MmaOverflowError}
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = _lib.ozgpu_last_error().decode()
+        raise _ERRORS.get(rc, OzmulError)(msg)
+
+
+# ------------------------------------------------------------------- types
+
+
+class ScheduleKind(enum.IntEnum):
+    FULL = 0      # kFull
+    REDUCED = 1   # kReduced
+
+
+class Accumulation(enum.IntEnum):
+    FLOAT_PER_PRODUCT = 0  # kFloatPerProduct
+    DIAGONAL_INTEGER = 1   # kDiagonalInteger
+    LEVELLED_EXACT = 2     # kLevelledExact
+
+
+class SliceMode(enum.IntEnum):
+    TRUNCATE = 0  # kTruncate
+    NEAREST = 1   # kNearest
+
+
+class BlockOrientation(enum.IntEnum):
+    ROWS = 0
+    COLUMNS = 1
+
+
+@dataclass(frozen=True)
+class MmaConfig:
+    """mma_sim.hpp:27-37."""
+    input_width: int = 7
+    acc_width: int = 31
+
+    @staticmethod
+    def int8_int32() -> "MmaConfig":
+        return MmaConfig(7, 31)
+
+    @staticmethod
+    def int4_int32() -> "MmaConfig":
+        return MmaConfig(3, 31)
+
+    def _c(self) -> _Cfg:
+        return _Cfg(self.input_width, self.acc_width)
+
+
+@dataclass
+class MultiplyPlan:
+    """scheme.hpp:77-88 (Schedule and LevelPlan folded in)."""
+    slices_a: int = 1
+    slices_b: int = 1
+    width: int = 7
+    schedule: ScheduleKind = ScheduleKind.REDUCED
+    diag_sum_limit: Optional[int] = None
+    strategy: Accumulation = Accumulation.LEVELLED_EXACT
+    mode: SliceMode = SliceMode.TRUNCATE
+    precision: int = 53
+    acc_bits_used: int = 0
+    levels: List[Tuple[int, int]] = field(default_factory=list)
+    level_inexact_adds: int = 0
+    psi: int = 0
+
+    @staticmethod
+    def _from_c(p: _Plan) -> "MultiplyPlan":
+        lv = [(p.levels[2 * i], p.levels[2 * i + 1]) for i in range(p.num_levels)]
+        return MultiplyPlan(p.slices_a, p.slices_b, p.width, ScheduleKind(p.schedule),
+                            p.diag_sum_limit if p.diag_sum_limit > 0 else None,
+                            Accumulation(p.strategy), SliceMode(p.mode), p.precision,
+                            p.acc_bits_used, lv, p.level_inexact_adds, p.psi)
+
+    def _c(self) -> _Plan:
+        p = _Plan()
+        p.slices_a, p.slices_b, p.width = self.slices_a, self.slices_b, self.width
+        p.schedule, p.strategy, p.mode = int(self.schedule), int(self.strategy), int(self.mode)
+        p.diag_sum_limit = self.diag_sum_limit or 0
+        p.precision, p.acc_bits_used = self.precision, self.acc_bits_used
+        p.num_levels = len(self.levels)
+        for i, (a, b) in enumerate(self.levels[:_MAX_LEVELS]):
+            p.levels[2 * i], p.levels[2 * i + 1] = a, b
+        p.level_inexact_adds, p.psi = self.level_inexact_adds, self.psi
+        return p
+
+
+@dataclass
+class Diagnostics:
+    """scheme.hpp:97-106."""
+    products: int = 0
+    integer_adds: int = 0
+    float_adds: int = 0
+    flushes: int = 0
+    realized_psi: int = 0
+    planned_psi: int = 0
+    width: int = 0
+    acc_bits_used: int = 0
+
+    @staticmethod
+    def _from_c(d: _Diag) -> "Diagnostics":
+        return Diagnostics(d.products, d.integer_adds, d.float_adds, d.flushes, d.realized_psi,
+                           d.planned_psi, d.width, d.acc_bits_used)
+
+
+@dataclass
+class MultiplyResult:
+    c: np.ndarray
+    diagnostics: Diagnostics
+
+
+@dataclass
+class SliceSelection:
+    """analysis.hpp:86-92."""
+    slices_a: int
+    slices_b: int
+    lhs: float
+    target: float
+    products: int
+
+
+@dataclass
+class SelectOptions:
+    """analysis.hpp:94-100."""
+    target: Optional[float] = None
+    schedule: ScheduleKind = ScheduleKind.REDUCED
+    strategy: Accumulation = Accumulation.LEVELLED_EXACT
+    acc_bits_used: int = 31
+    precision: int = 53
+
+
+@dataclass
+class ScalingProfile:
+    """analysis.hpp:30-38 (scalar part)."""
+    kappa_a: float
+    kappa_b: float
+    a_has_zero_block: bool
+    b_has_zero_block: bool
+
+
+@dataclass
+class SlicedMatrix:
+    """slicing.hpp:44-63: slices[l] is the l-th (most significant first) int64 slice."""
+    orientation: BlockOrientation
+    mode: SliceMode
+    width: int
+    scale_exponents: np.ndarray
+    slices: np.ndarray  # [count, rows, cols] int64
+
+    def slice_count(self) -> int:
+        return int(self.slices.shape[0])
+
+    def end_bit(self, index: int) -> int:
+        last = (index + 1) * self.width
+        return last - 1 if self.mode == SliceMode.NEAREST else last
+
+
+# ----------------------------------------------------------------- context
+
+_ctx_lock = threading.Lock()
+
+
+def _ctx(device: Optional[int] = None) -> int:
+    if device is None:
+        device = int(os.environ.get("OZGPU_DEVICE", "0"))
+    with _ctx_lock:
+        c = _lib.ozgpu_default_context(device)
+    if not c:
+        raise DeviceError(_lib.ozgpu_last_error().decode())
+    return c
+
+
+def kernel_launches(device: Optional[int] = None) -> int:
+    """Kernels this library launched through the default context so far."""
+    return int(_lib.ozgpu_kernel_launches(_ctx(device)))
+
+
+def version() -> str:
+    return _lib.ozgpu_version().decode()
+
+
+def _f64(x) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    if a.ndim != 2:
+        raise InvalidArgument("expected a 2-D matrix")
+    return a
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(_DP)
+
+
+# ------------------------------------------------------------------ plan
+
+
+def optimal_slice_width(cfg: MmaConfig, k: int) -> int:
+    out = ctypes.c_int()
+    _check(_lib.ozgpu_optimal_slice_width(cfg._c(), k, ctypes.byref(out)))
+    return out.value
+
+
+def max_inner_dim(cfg: MmaConfig) -> int:
+    out = _I64()
+    _check(_lib.ozgpu_max_inner_dim(cfg._c(), ctypes.byref(out)))
+    return out.value
+
+
+def chi(slices_a: int, slices_b: int) -> int:
+    out = _I64()
+    _check(_lib.ozgpu_chi(slices_a, slices_b, ctypes.byref(out)))
+    return out.value
+
+
+def spare_carries(first_diag: int, last_diag: int, width: int) -> int:
+    out = _I64()
+    _check(_lib.ozgpu_spare_carries(first_diag, last_diag, width, ctypes.byref(out)))
+    return out.value
+
+
+def plan_levels(precision: int, width: int, acc_bits_used: int, num_diagonals: int):
+    """Returns (levels, inexact_adds) as scheme.cpp:64-95."""
+    p = _Plan()
+    _check(_lib.ozgpu_plan_levels(precision, width, acc_bits_used, num_diagonals, ctypes.byref(p)))
+    return [(p.levels[2 * i], p.levels[2 * i + 1]) for i in range(p.num_levels)], \
+        p.level_inexact_adds
+
+
+def diagonal_flush_threshold(cfg: MmaConfig, width: int, k: int) -> int:
+    out = _I64()
+    _check(_lib.ozgpu_diagonal_flush_threshold(cfg._c(), width, k, ctypes.byref(out)))
+    return out.value
+
+
+def make_plan(cfg: MmaConfig, k: int, slices_a: int, slices_b: int,
+              schedule: ScheduleKind = ScheduleKind.REDUCED,
+              strategy: Accumulation = Accumulation.LEVELLED_EXACT,
+              mode: SliceMode = SliceMode.TRUNCATE, precision: int = 53) -> MultiplyPlan:
+    p = _Plan()
+    _check(_lib.ozgpu_make_plan(cfg._c(), k, slices_a, slices_b, int(schedule), int(strategy),
+                                int(mode), precision, ctypes.byref(p)))
+    return MultiplyPlan._from_c(p)
+
+
+# ------------------------------------------------------------- estimator
+
+
+def select_slices(kappa_a: float, kappa_b: float, width: int, u: float, s_max: int,
+                  options: Optional[SelectOptions] = None) -> SliceSelection:
+    o = options or SelectOptions()
+    s = _Sel()
+    rc = _lib.ozgpu_select_slices(kappa_a, kappa_b, width, u, s_max, int(o.target is not None),
+                                  o.target if o.target is not None else 0.0, int(o.schedule),
+                                  int(o.strategy), o.acc_bits_used, o.precision, ctypes.byref(s))
+    if rc == 4:
+        raise SelectionInfeasible(_lib.ozgpu_last_error().decode(), s.gap, s.lhs, s.target)
+    _check(rc)
+    return SliceSelection(s.slices_a, s.slices_b, s.lhs, s.target, s.products)
+
+
+def scaling_profile(a, b, device: Optional[int] = None) -> ScalingProfile:
+    a, b = _f64(a), _f64(b)
+    if a.shape[1] != b.shape[0]:
+        raise InvalidArgument("scaling_profile: shape mismatch")
+    out = _Prof()
+    _check(_lib.ozgpu_scaling_profile(_ctx(device), a.shape[0], a.shape[1], b.shape[1], _dp(a),
+                                      a.shape[1], _dp(b), b.shape[1], ctypes.byref(out)))
+    return ScalingProfile(out.kappa_a, out.kappa_b, bool(out.a_has_zero_block),
+                          bool(out.b_has_zero_block))
+
+
+# ------------------------------------------------------------------ GEMM
+
+
+def multiply(a, b, cfg: MmaConfig, plan: MultiplyPlan, device: Optional[int] = None,
+             out: Optional[np.ndarray] = None) -> MultiplyResult:
+    """scheme.cpp:219-361 on the GPU (host arrays in, host array out).
+
+    `out` (optional) receives C in place, e.g. a pinned buffer."""
+    a, b = _f64(a), _f64(b)
+    if a.shape[1] != b.shape[0]:
+        raise InvalidArgument("multiply: shape mismatch")
+    m, k = a.shape
+    n = b.shape[1]
+    if out is not None:
+        if out.shape != (m, n) or out.dtype != np.float64 or not out.flags.c_contiguous:
+            raise InvalidArgument("multiply: out must be a contiguous float64 m x n array")
+        c = out
+    else:
+        c = np.empty((m, n), dtype=np.float64)
+    d = _Diag()
+    pc = plan._c()
+    _check(_lib.ozgpu_dgemm(_ctx(device), m, n, k, _dp(a), k, _dp(b), n, _dp(c), n, cfg._c(),
+                            ctypes.byref(pc), ctypes.byref(d)))
+    return MultiplyResult(c, Diagnostics._from_c(d))
+
+
+def multiply_axpby(alpha: float, a, b, beta: float, c, cfg: MmaConfig, plan: MultiplyPlan,
+                   device: Optional[int] = None) -> MultiplyResult:
+    """scheme.cpp:363-372."""
+    a, b, c = _f64(a), _f64(b), _f64(c)
+    if c.shape != (a.shape[0], b.shape[1]) or a.shape[1] != b.shape[0]:
+        raise InvalidArgument("multiply_axpby: shape mismatch")
+    m, k = a.shape
+    n = b.shape[1]
+    out = np.empty((m, n), dtype=np.float64)
+    d = _Diag()
+    pc = plan._c()
+    _check(_lib.ozgpu_dgemm_axpby(_ctx(device), m, n, k, alpha, _dp(a), k, _dp(b), n, beta,
+                                  _dp(c), n, _dp(out), n, cfg._c(), ctypes.byref(pc),
+                                  ctypes.byref(d)))
+    return MultiplyResult(out, Diagnostics._from_c(d))
+
+
+def multiply_device(m: int, n: int, k: int, a_ptr: int, lda: int, b_ptr: int, ldb: int,
+                    c_ptr: int, ldc: int, cfg: MmaConfig, plan: MultiplyPlan,
+                    stream: int = 0, status_ptr: int = 0,
+                    device: Optional[int] = None) -> Diagnostics:
+    """Device-resident multiply (ozgpu_dgemm_device): enqueues on `stream`, no sync."""
+    d = _Diag()
+    pc = plan._c()
+    _check(_lib.ozgpu_dgemm_device(_ctx(device), m, n, k, a_ptr, lda, b_ptr, ldb, c_ptr, ldc,
+                                   cfg._c(), ctypes.byref(pc), stream or None,
+                                   status_ptr or None, ctypes.byref(d)))
+    return Diagnostics._from_c(d)
+
+
+# ------------------------------------------------------------ debug hooks
+
+
+def _split(x, width: int, count: int, mode: SliceMode, orientation: int,
+           device: Optional[int]) -> SlicedMatrix:
+    x = _f64(x)
+    rows, cols = x.shape
+    slices = np.zeros((max(count, 0), rows, cols), dtype=np.int64)
+    scales = np.zeros(rows if orientation == 0 else cols, dtype=np.int32)
+    _check(_lib.ozgpu_split(_ctx(device), orientation, rows, cols, _dp(x), cols, width, count,
+                            int(mode), slices.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                            scales.ctypes.data_as(ctypes.POINTER(ctypes.c_int))))
+    return SlicedMatrix(BlockOrientation(orientation), SliceMode(mode), width, scales, slices)
+
+
+def split_rows(a, width: int, count: int, mode: SliceMode = SliceMode.TRUNCATE,
+               device: Optional[int] = None) -> SlicedMatrix:
+    """slicing.cpp:67-132, one scale per row, on the GPU."""
+    return _split(a, width, count, mode, 0, device)
+
+
+def split_cols(b, width: int, count: int, mode: SliceMode = SliceMode.TRUNCATE,
+               device: Optional[int] = None) -> SlicedMatrix:
+    """slicing.cpp:67-132, one scale per column, on the GPU."""
+    return _split(b, width, count, mode, 1, device)
+
+
+def integer_gemm(x, y, cfg: MmaConfig, c=None, device: Optional[int] = None) -> np.ndarray:
+    """mma_sim.cpp:76-125 on the GPU (tcgen05 int8 path when provably exact)."""
+    x = np.ascontiguousarray(np.asarray(x, dtype=np.int64))
+    y = np.ascontiguousarray(np.asarray(y, dtype=np.int64))
+    if x.shape[1] != y.shape[0]:
+        raise InvalidArgument("integer_gemm: shape mismatch")
+    m, k = x.shape
+    n = y.shape[1]
+    cp = None
+    if c is not None:
+        cp = np.ascontiguousarray(np.asarray(c, dtype=np.int64))
+        if cp.shape != (m, n):
+            raise InvalidArgument("integer_gemm: accumulator shape mismatch")
+    out = np.zeros((m, n), dtype=np.int64)
+    P = ctypes.POINTER(ctypes.c_int64)
+    _check(_lib.ozgpu_integer_gemm(_ctx(device), m, k, n, x.ctypes.data_as(P),
+                                   y.ctypes.data_as(P),
+                                   cp.ctypes.data_as(P) if cp is not None else None,
+                                   out.ctypes.data_as(P), cfg._c()))
+    return out
+
+
+# -------------------------------------------------------------- generators
+
+
+def random_uniform(m: int, n: int, seed: int, lo: float = 0.0, hi: float = 1.0) -> np.ndarray:
+    """generators.cpp:176-182 (identical bytes to the reference generator)."""
+    out = np.empty((m, n), dtype=np.float64)
+    _lib.ozgpu_random_uniform(m, n, seed, lo, hi, _dp(out))
+    return out
+
+
+def gen_kappa_d(n: int, kappa_d: float, seed: int, rotate: bool):
+    """generators.cpp:103-140."""
+    a = np.empty((n, n), dtype=np.float64)
+    b = np.empty((n, n), dtype=np.float64)
+    _lib.ozgpu_gen_kappa_d(n, kappa_d, seed, int(rotate), _dp(a), _dp(b))
+    return a, b
+
+
+# ------------------------------------------------------------ stage timing
+
+_sig("ozgpu_set_stage_timing", ctypes.c_int, _P, ctypes.c_int)
+_sig("ozgpu_stage_times", ctypes.c_int, _P, ctypes.POINTER(ctypes.c_double),
+     ctypes.POINTER(_I64), ctypes.c_int)
+
+
+def set_stage_timing(enable: bool, device: Optional[int] = None) -> None:
+    """Record CUDA events around slicing / pair GEMMs / combine of each multiply."""
+    _check(_lib.ozgpu_set_stage_timing(_ctx(device), int(enable)))
+
+
+def stage_times(reset: bool = True, device: Optional[int] = None):
+    """(slicing_ms, gemm_ms, combine_ms, calls) accumulated since the last reset."""
+    ms = (ctypes.c_double * 3)()
+    calls = _I64()
+    _check(_lib.ozgpu_stage_times(_ctx(device), ms, ctypes.byref(calls), int(reset)))
+    return ms[0], ms[1], ms[2], calls.value

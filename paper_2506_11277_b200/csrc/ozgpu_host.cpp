@@ -1,0 +1,975 @@
+// Host orchestration and C-ABI of the B200-native Ozaki-I FP64 GEMM.
+//
+// ozgpu_dgemm* replace the reference's ozmul::multiply (proj/src/scheme.cpp:
+// 219-361): validation in the reference's order, then three GPU stages on one
+// stream -- slicing (HBM-bound), tcgen05 int8 pair GEMMs (tensor-bound) and
+// the exact combine -- with no CPU fallback: a missing device is an error.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "ozgpu.h"
+#include "ozgpu_internal.h"
+#include "ozgpu_plan.h"
+
+namespace ozgpu {
+namespace {
+
+thread_local std::string g_error;
+
+struct DeviceError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define OZ_CUDA(call)                                                                    \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      throw DeviceError(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " + \
+                        #call);                                                          \
+  } while (0)
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return OZGPU_OK;
+  } catch (const SelectionInfeasibleError& e) {
+    g_error = e.what();
+    return OZGPU_INFEASIBLE;
+  } catch (const OverflowError& e) {
+    g_error = e.what();
+    return OZGPU_OVERFLOW;
+  } catch (const std::invalid_argument& e) {
+    g_error = e.what();
+    return OZGPU_INVALID_ARGUMENT;
+  } catch (const std::domain_error& e) {
+    g_error = e.what();
+    return OZGPU_DOMAIN_ERROR;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return OZGPU_DEVICE_ERROR;
+  }
+}
+
+// A grow-only device allocation.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void* get(size_t want) {
+    if (want > bytes) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      bytes = 0;
+      if (want) {
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e != cudaSuccess) {
+          cudaGetLastError();
+          throw DeviceError("device allocation of " + std::to_string(want) +
+                            " bytes failed: " + cudaGetErrorString(e));
+        }
+      }
+      bytes = want;
+    }
+    return p;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+}  // namespace
+}  // namespace ozgpu
+
+struct ozgpu_ctx {
+  int device = 0;
+  int num_sms = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  std::atomic<int64_t> launches{0};
+  ozgpu::EncodeTiledFn encode = nullptr;
+  // workspace
+  ozgpu::DevBuf slices_a, slices_b, qa, qb, colmax, colmin, status, planes, chunks, psi;
+  ozgpu::DevBuf in_a, in_b, io_c, in_c2, ratios, i64a, i64b, i64c, i64o, ovf;
+  std::vector<ozgpu::ChunkDesc> host_chunks;
+  // stage timing (ozgpu_set_stage_timing)
+  bool timing = false;
+  std::vector<std::array<cudaEvent_t, 4>> pending_events;
+  std::vector<cudaEvent_t> event_pool;
+  double stage_ms[3] = {0, 0, 0};
+  int64_t timed_calls = 0;
+};
+
+namespace ozgpu {
+namespace {
+
+void init_ctx(ozgpu_ctx* ctx, int device) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    throw DeviceError("no CUDA device available (the Ozaki-I path has no CPU fallback)");
+  }
+  if (device < 0 || device >= count) throw std::invalid_argument("ozgpu_create: bad device index");
+  cudaDeviceProp prop{};
+  OZ_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10 || prop.minor != 0)
+    throw DeviceError("device " + std::to_string(device) + " (" + prop.name + ", sm_" +
+                      std::to_string(prop.major) + std::to_string(prop.minor) +
+                      ") is not sm_100: kernels are built for sm_100a only");
+  ctx->device = device;
+  ctx->num_sms = prop.multiProcessorCount;
+  OZ_CUDA(cudaSetDevice(device));
+  OZ_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  OZ_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess)
+    throw DeviceError("cuTensorMapEncodeTiled unavailable from the driver");
+  ctx->encode = reinterpret_cast<EncodeTiledFn>(fn);
+}
+
+// 3-D int8 tensor map over slices [count][rows][kp], box {128, box_rows, 1},
+// 128-byte swizzle (matches the UMMA SW128 K-major descriptor).
+CUtensorMap make_slice_map(ozgpu_ctx* ctx, const void* base, int64_t kp, int64_t rows,
+                           int count, int box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(kp), static_cast<cuuint64_t>(rows),
+                        static_cast<cuuint64_t>(count)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(kp), static_cast<cuuint64_t>(kp * rows)};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(kBlockK), static_cast<cuuint32_t>(box_rows), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = ctx->encode(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw DeviceError("cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return m;
+}
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+cudaEvent_t take_event(ozgpu_ctx* ctx) {
+  if (!ctx->event_pool.empty()) {
+    cudaEvent_t e = ctx->event_pool.back();
+    ctx->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  OZ_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+// Resolves pending stage events into ctx->stage_ms (caller holds ctx->mu).
+void drain_events(ozgpu_ctx* ctx) {
+  for (auto& ev : ctx->pending_events) {
+    OZ_CUDA(cudaEventSynchronize(ev[3]));
+    for (int s = 0; s < 3; ++s) {
+      float ms = 0.f;
+      OZ_CUDA(cudaEventElapsedTime(&ms, ev[s], ev[s + 1]));
+      ctx->stage_ms[s] += ms;
+    }
+    ++ctx->timed_calls;
+    for (cudaEvent_t e : ev) ctx->event_pool.push_back(e);
+  }
+  ctx->pending_events.clear();
+}
+
+// Chunking of the scheduled pairs.  Levelled-exact: the int32 capacity of the
+// tensor-core accumulator bounds the pairs per chunk (the result is order-
+// independent).  Float-per-product: one pair per chunk.  Diagonal-integer:
+// the reference's flush grouping (scheme.cpp:281-313), split further only if
+// a reference chunk could exceed int32 (flush_after marks the end of a
+// reference chunk).
+struct ChunkPlan {
+  std::vector<ChunkDesc> chunks;
+  int diagonals = 0;
+};
+
+ChunkPlan build_chunks(const ozgpu_plan& p, const ozgpu_mma_config& cfg, int64_t k) {
+  ChunkPlan cp;
+  cp.diagonals = max_diag_sum(p) - 1;
+  const int t = p.width;
+  const int64_t maxs = (int64_t{1} << t) - 1;
+  const int64_t prod_bound = k * maxs * maxs;
+  int64_t cap32 = std::max<int64_t>(1, (int64_t{2147483647}) / std::max<int64_t>(prod_bound, 1));
+  int64_t ref_flush = 0;
+  if (p.strategy == 1) {
+    ref_flush = diagonal_flush_threshold(cfg, t, k);
+    if (p.precision < cfg.acc_width)
+      ref_flush = std::min(ref_flush, int64_t{1} << std::max(0, p.precision - 2 * t - ceil_log2(k)));
+  }
+  for (int d = 0; d < cp.diagonals; ++d) {
+    int w = diagonal_width(d, p.slices_a, p.slices_b);
+    if (w == 0) continue;
+    int l0 = diagonal_first_l(d, p.slices_b);
+    int shift = (cp.diagonals - 1 - d) * t;
+    if (p.strategy == 2) {
+      for (int s = 0; s < w; s += static_cast<int>(cap32)) {
+        int np = static_cast<int>(std::min<int64_t>(cap32, w - s));
+        cp.chunks.push_back({d, l0 + s, np, shift, 1});
+      }
+    } else if (p.strategy == 0) {
+      for (int s = 0; s < w; ++s) cp.chunks.push_back({d, l0 + s, 1, shift, 1});
+    } else {
+      for (int s = 0; s < w; s += static_cast<int>(std::min<int64_t>(ref_flush, w))) {
+        int ref_len = static_cast<int>(std::min<int64_t>(ref_flush, w - s));
+        for (int u = 0; u < ref_len; u += static_cast<int>(cap32)) {
+          int np = static_cast<int>(std::min<int64_t>(cap32, ref_len - u));
+          cp.chunks.push_back({d, l0 + s + u, np, shift, u + np >= ref_len ? 1 : 0});
+        }
+      }
+    }
+  }
+  return cp;
+}
+
+// Diagnostics exactly as the reference accumulates them (scheme.cpp:246-359).
+ozgpu_diag make_diag(const ozgpu_plan& p, const ozgpu_mma_config& cfg, int64_t m, int64_t n,
+                     int64_t k, long long realized_psi) {
+  ozgpu_diag d{};
+  d.width = p.width;
+  d.acc_bits_used = 2 * p.width + ceil_log2(k);
+  d.planned_psi = p.psi;
+  const uint64_t mn = static_cast<uint64_t>(m) * static_cast<uint64_t>(n);
+  const int diagonals = max_diag_sum(p) - 1;
+  uint64_t products = 0, iadds = 0, fadds = 0, flushes = 0;
+  if (p.strategy == 1) {
+    int64_t flush = diagonal_flush_threshold(cfg, p.width, k);
+    if (p.precision < cfg.acc_width)
+      flush = std::min(flush, int64_t{1} << std::max(0, p.precision - d.acc_bits_used));
+    for (int dd = 0; dd < diagonals; ++dd) {
+      int64_t w = diagonal_width(dd, p.slices_a, p.slices_b);
+      int64_t chunks = 0;
+      for (int64_t taken = 0; taken < w;) {
+        int64_t in_chain = std::min<int64_t>(flush, w - taken);
+        products += in_chain;
+        iadds += static_cast<uint64_t>(k - 1) * mn + static_cast<uint64_t>(in_chain - 1) *
+                                                          static_cast<uint64_t>(k) * mn;
+        fadds += 1;
+        taken += in_chain;
+        ++chunks;
+      }
+      if (chunks > 1) flushes += chunks - 1;
+    }
+  } else {
+    for (int dd = 0; dd < diagonals; ++dd) {
+      int64_t w = diagonal_width(dd, p.slices_a, p.slices_b);
+      products += w;
+      iadds += static_cast<uint64_t>(w) * static_cast<uint64_t>(k - 1) * mn;
+      fadds += w;
+    }
+    if (p.strategy == 2) {
+      // level count as multiply() re-derives it when the plan's levels do
+      // not tile the diagonals (scheme.cpp:316-320)
+      int nlev = p.num_levels;
+      if (nlev == 0 || p.levels[0] != 0 || p.levels[2 * (nlev - 1) + 1] != diagonals - 1)
+        nlev = static_cast<int>(plan_levels(p.precision, p.width, d.acc_bits_used, diagonals)
+                                    .levels.size());
+      if (nlev > 1) fadds += nlev - 1;
+    }
+  }
+  d.products = static_cast<int64_t>(products);
+  d.integer_adds = static_cast<int64_t>(iadds);
+  d.float_adds = static_cast<int64_t>(fadds);
+  d.flushes = static_cast<int64_t>(flushes);
+  d.realized_psi = realized_psi;
+  return d;
+}
+
+struct ValidationResult {
+  bool capacity_error = false;
+  bool precision_error = false;
+  std::string message;
+};
+
+// scheme.cpp:221-239 (minus the clean-input scan, which runs on the GPU)
+ValidationResult host_validation(const ozgpu_mma_config& cfg, const ozgpu_plan& p, int64_t k) {
+  validate_cfg(cfg);
+  ValidationResult v;
+  const int t = p.width;
+  if (k >= 1) {
+    if (2 * t + ceil_log2(k) > cfg.acc_width) {
+      v.capacity_error = true;
+      v.message = "multiply: inner dimension " + std::to_string(k) +
+                  " exceeds the capacity limit " + std::to_string(max_inner_dim(cfg)) +
+                  " of this unit";
+    } else if (p.precision < 2 * t + ceil_log2(k)) {
+      v.precision_error = true;
+      v.message = "multiply: accumulation format too narrow for exact conversion; needs " +
+                  std::to_string(2 * t + ceil_log2(k)) + " bits";
+    }
+  }
+  return v;
+}
+
+int exact_words(int diagonals, int width, size_t nchunks) {
+  int bits = (diagonals - 1) * width + 32 + ceil_log2(static_cast<int64_t>(nchunks) + 1) + 2;
+  int w = (bits + 63) / 64;
+  for (int cand : {2, 3, 4, 6, 8, 12, 16})
+    if (w <= cand) return cand;
+  throw std::invalid_argument("multiply: exact accumulator wider than 1024 bits");
+}
+
+// The device-resident core of multiply(): everything is enqueued on `st`.
+// Returns the realized psi device pointer (sequential strategies) or null.
+int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* da, int64_t lda,
+                  const double* db, int64_t ldb, double* dc, int64_t ldc,
+                  const ozgpu_mma_config& cfg, const ozgpu_plan& p, cudaStream_t st,
+                  int* dev_status, bool axpby, double alpha, double beta, const double* dcin,
+                  int64_t ldcin) {
+  int64_t launches = 0;
+  std::array<cudaEvent_t, 4> ev{};
+  if (ctx->timing) {
+    for (auto& e : ev) e = take_event(ctx);
+    OZ_CUDA(cudaEventRecord(ev[0], st));
+  }
+  const int t = p.width;
+  if (t > 7)
+    throw std::invalid_argument("multiply: slice width " + std::to_string(t) +
+                                " exceeds the int8 tensor-core operand (t <= 7)");
+  if (t < 1 || t > 62) throw std::invalid_argument("split: width out of range");
+  if (p.mode == 1 && t < 2) throw std::invalid_argument("split: nearest mode needs width >= 2");
+  const int sa = p.slices_a, sb = p.slices_b;
+  const int64_t kp = round_up(k, kKPad);
+  ChunkPlan cp = build_chunks(p, cfg, k);
+
+  int8_t* slA = static_cast<int8_t*>(ctx->slices_a.get(static_cast<size_t>(sa) * m * kp + 1));
+  int8_t* slB = static_cast<int8_t*>(ctx->slices_b.get(static_cast<size_t>(sb) * n * kp + 1));
+  int* qa = static_cast<int*>(ctx->qa.get(sizeof(int) * (m + 1)));
+  int* qb = static_cast<int*>(ctx->qb.get(sizeof(int) * (n + 1)));
+  auto* colmax = static_cast<unsigned long long*>(ctx->colmax.get(8 * (n + 1)));
+  int* status = dev_status ? dev_status : static_cast<int*>(ctx->status.get(sizeof(int)));
+  OZ_CUDA(cudaMemsetAsync(status, 0, sizeof(int), st));
+
+  OZ_CUDA(launch_slice_rows(da, lda, m, k, kp, t, sa, p.mode, slA, 0, qa, status, st, &launches));
+  OZ_CUDA(launch_slice_cols(db, ldb, k, n, kp, t, sb, p.mode, slB, 0, qb, colmax, status, st,
+                            &launches));
+  if (ctx->timing) OZ_CUDA(cudaEventRecord(ev[1], st));
+
+  int* psi_dev = nullptr;
+  if (m > 0 && n > 0 && !cp.chunks.empty()) {
+    const int64_t ldp = round_up(n, 4);
+    const int64_t plane = m * ldp;
+    int32_t* planes = static_cast<int32_t*>(
+        ctx->planes.get(sizeof(int32_t) * static_cast<size_t>(plane) * cp.chunks.size()));
+    ChunkDesc* dchunks =
+        static_cast<ChunkDesc*>(ctx->chunks.get(sizeof(ChunkDesc) * cp.chunks.size()));
+    OZ_CUDA(cudaMemcpyAsync(dchunks, cp.chunks.data(), sizeof(ChunkDesc) * cp.chunks.size(),
+                            cudaMemcpyHostToDevice, st));
+    // keep the host copy alive until the stream consumes it
+    ctx->host_chunks = cp.chunks;
+
+    CUtensorMap tma = make_slice_map(ctx, slA, kp, m, sa, kBlockM);
+    CUtensorMap tmb = make_slice_map(ctx, slB, kp, n, sb, 256);
+    GemmArgs g{};
+    g.chunks = dchunks;
+    g.nchunks = static_cast<int>(cp.chunks.size());
+    g.m = static_cast<int>(m);
+    g.n = static_cast<int>(n);
+    g.kblocks = static_cast<int>(kp / kBlockK);
+    g.tiles_m = static_cast<int>((m + kBlockM - 1) / kBlockM);
+    g.tiles_n = static_cast<int>((n + 255) / 256);
+    g.total_units = g.tiles_m * g.tiles_n * g.nchunks;
+    g.planes = planes;
+    g.plane_stride = plane;
+    g.ldp = ldp;
+    OZ_CUDA(launch_gemm_i8(&tma, &tmb, g, ctx->num_sms, st, &launches));
+    if (ctx->timing) OZ_CUDA(cudaEventRecord(ev[2], st));
+
+    CombineArgs c{};
+    c.planes = planes;
+    c.chunks = dchunks;
+    c.nchunks = g.nchunks;
+    c.plane_stride = plane;
+    c.ldp = ldp;
+    c.qa = qa;
+    c.qb = qb;
+    c.m = static_cast<int>(m);
+    c.n = static_cast<int>(n);
+    c.width = t;
+    c.diagonals = cp.diagonals;
+    c.mode = p.mode;
+    c.w_last = -static_cast<long>(cp.diagonals + 1) * t + (p.mode == 1 ? 2 : 0);
+    c.c = dc;
+    c.ldc = ldc;
+    c.axpby = axpby ? 1 : 0;
+    c.alpha = alpha;
+    c.beta = beta;
+    c.cin = dcin;
+    c.ldcin = ldcin;
+    if (p.strategy == 2) {
+      OZ_CUDA(launch_combine_exact(c, exact_words(cp.diagonals, t, cp.chunks.size()), st,
+                                   &launches));
+    } else {
+      psi_dev = static_cast<int*>(ctx->psi.get(sizeof(int)));
+      OZ_CUDA(cudaMemsetAsync(psi_dev, 0, sizeof(int), st));
+      c.realized_psi = psi_dev;
+      OZ_CUDA(launch_combine_sequential(c, st, &launches));
+    }
+  } else if (m > 0 && n > 0) {
+    // no scheduled products: C = 0 (+ beta*C for axpby) -- cannot happen for
+    // valid plans (max_diag_sum >= 2), kept for completeness
+    OZ_CUDA(cudaMemset2DAsync(dc, ldc * sizeof(double), 0, n * sizeof(double), m, st));
+  }
+  if (ctx->timing) {
+    if (!(m > 0 && n > 0 && !cp.chunks.empty())) OZ_CUDA(cudaEventRecord(ev[2], st));
+    OZ_CUDA(cudaEventRecord(ev[3], st));
+    ctx->pending_events.push_back(ev);
+  }
+  ctx->launches += launches;
+  return psi_dev;
+}
+
+// Copies a row-major host matrix (ld) into a dense device buffer (ld = cols).
+void h2d(void* dst, const double* src, int64_t rows, int64_t cols, int64_t ld, cudaStream_t st) {
+  if (rows == 0 || cols == 0) return;
+  OZ_CUDA(cudaMemcpy2DAsync(dst, cols * sizeof(double), src, ld * sizeof(double),
+                            cols * sizeof(double), rows, cudaMemcpyHostToDevice, st));
+}
+void d2h(double* dst, int64_t ld, const void* src, int64_t rows, int64_t cols, cudaStream_t st) {
+  if (rows == 0 || cols == 0) return;
+  OZ_CUDA(cudaMemcpy2DAsync(dst, ld * sizeof(double), src, cols * sizeof(double),
+                            cols * sizeof(double), rows, cudaMemcpyDeviceToHost, st));
+}
+
+void check_plan(const ozgpu_plan* plan) {
+  if (!plan) throw std::invalid_argument("multiply: null plan");
+  if (plan->slices_a < 1 || plan->slices_b < 1)
+    throw std::invalid_argument("split: need at least one slice");
+  if (plan->strategy < 0 || plan->strategy > 2)
+    throw std::invalid_argument("multiply: unknown accumulation strategy");
+}
+
+// Host-pointer multiply / multiply_axpby.
+void host_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda,
+                   const double* b, int64_t ldb, double* c, int64_t ldc,
+                   const ozgpu_mma_config& cfg, const ozgpu_plan& p, ozgpu_diag* diag,
+                   bool axpby, double alpha, double beta, const double* cin, int64_t ldcin) {
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  OZ_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  ValidationResult v = host_validation(cfg, p, k);
+  double* da = static_cast<double*>(ctx->in_a.get(sizeof(double) * m * k + 8));
+  double* db = static_cast<double*>(ctx->in_b.get(sizeof(double) * k * n + 8));
+  h2d(da, a, m, k, lda, st);
+  h2d(db, b, k, n, ldb, st);
+  if (k < 1 || v.capacity_error || v.precision_error) {
+    // the clean-input check precedes these errors (scheme.cpp:223-239)
+    int* status = static_cast<int*>(ctx->status.get(sizeof(int)));
+    OZ_CUDA(cudaMemsetAsync(status, 0, sizeof(int), st));
+    int64_t launches = 0;
+    auto* colmax = static_cast<unsigned long long*>(ctx->colmax.get(8 * (n + 1)));
+    int* qa = static_cast<int*>(ctx->qa.get(sizeof(int) * (m + 1)));
+    int* qb = static_cast<int*>(ctx->qb.get(sizeof(int) * (n + 1)));
+    int64_t kp8 = round_up(std::max<int64_t>(k, 1), 8);
+    int8_t* sA = static_cast<int8_t*>(ctx->slices_a.get(static_cast<size_t>(m) * kp8 + 1));
+    int8_t* sB = static_cast<int8_t*>(ctx->slices_b.get(static_cast<size_t>(n) * kp8 + 1));
+    if (k >= 1) {
+      OZ_CUDA(launch_slice_rows(da, k, m, k, kp8, 1, 1, 0, sA, 0, qa, status, st, &launches));
+      OZ_CUDA(launch_slice_cols(db, n, k, n, kp8, 1, 1, 0, sB, 0, qb, colmax, status, st,
+                                &launches));
+    }
+    int hs = 0;
+    OZ_CUDA(cudaMemcpyAsync(&hs, status, sizeof(int), cudaMemcpyDeviceToHost, st));
+    OZ_CUDA(cudaStreamSynchronize(st));
+    ctx->launches += launches;
+    if (hs) throw std::invalid_argument("multiply: inputs must be finite with no negative zeros");
+    if (k < 1) throw std::invalid_argument("multiply: empty inner dimension");
+    throw std::domain_error(v.message);
+  }
+  double* dc = static_cast<double*>(ctx->io_c.get(sizeof(double) * m * n + 8));
+  const double* dcin = nullptr;
+  if (axpby) {
+    double* t = static_cast<double*>(ctx->in_c2.get(sizeof(double) * m * n + 8));
+    h2d(t, cin, m, n, ldcin, st);
+    dcin = t;
+  }
+  int* psi_dev = run_multiply(ctx, m, n, k, da, k, db, n, dc, n, cfg, p, st, nullptr, axpby,
+                              alpha, beta, dcin, n);
+  d2h(c, ldc, dc, m, n, st);
+  int hs = 0, hpsi = 0;
+  OZ_CUDA(cudaMemcpyAsync(&hs, ctx->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (psi_dev) OZ_CUDA(cudaMemcpyAsync(&hpsi, psi_dev, sizeof(int), cudaMemcpyDeviceToHost, st));
+  OZ_CUDA(cudaStreamSynchronize(st));
+  if (hs) throw std::invalid_argument("multiply: inputs must be finite with no negative zeros");
+  if (diag) *diag = make_diag(p, cfg, m, n, k, hpsi);
+}
+
+ozgpu_ctx* g_default[64];
+std::mutex g_default_mu;
+
+}  // namespace
+
+// analysis.cpp:142-207
+ozgpu_selection select_slices(double kappa_a, double kappa_b, int width, double u, int s_max,
+                              bool has_target, double target, int schedule, int strategy,
+                              int acc_bits_used, int precision) {
+  if (width < 1 || s_max < 1 || s_max > 64 || !(u > 0.0) || !(u < 1.0))
+    throw std::invalid_argument("select_slices: bad arguments");
+  if (!(kappa_a > 0.0) || !(kappa_b > 0.0))
+    throw std::invalid_argument("select_slices: kappas must be positive");
+  bool found = false;
+  ozgpu_selection best{};
+  double best_lhs_any = std::numeric_limits<double>::infinity();
+  double target_at_best = 0.0;
+  for (int sa = 1; sa <= s_max; ++sa)
+    for (int sb = 1; sb <= s_max; ++sb) {
+      double lhs = std::ldexp(kappa_a, -sa * width) + std::ldexp(kappa_b, -sb * width);
+      double tgt;
+      if (has_target) {
+        tgt = target;
+      } else {
+        int diagonals = schedule == 0 ? sa + sb - 1 : std::max(sa, sb);
+        long long psi;
+        if (strategy == 2)
+          psi = plan_levels(precision, width, acc_bits_used, diagonals).inexact_adds;
+        else if (strategy == 1)
+          psi = diagonals - 1;
+        else
+          psi = (schedule == 0 ? static_cast<int64_t>(sa) * sb : chi(sa, sb)) - 1;
+        tgt = gamma_factor(std::max(psi, 1LL), u);
+      }
+      if (lhs < best_lhs_any) {
+        best_lhs_any = lhs;
+        target_at_best = tgt;
+      }
+      if (lhs > tgt) continue;
+      int64_t cost = chi(sa, sb);
+      bool better;
+      if (!found)
+        better = true;
+      else if (cost != best.products)
+        better = cost < best.products;
+      else if (std::max(sa, sb) != std::max(best.slices_a, best.slices_b))
+        better = std::max(sa, sb) < std::max(best.slices_a, best.slices_b);
+      else
+        better = sa < best.slices_a;
+      if (better) {
+        best = {sa, sb, lhs, tgt, cost, 0.0};
+        found = true;
+      }
+    }
+  if (!found) {
+    double gap = best_lhs_any / std::max(target_at_best, std::numeric_limits<double>::min());
+    throw SelectionInfeasibleError(
+        "select_slices: no feasible pair within s_max = " + std::to_string(s_max) +
+            "; best achievable term exceeds the target by a factor " + std::to_string(gap),
+        gap, best_lhs_any, target_at_best);
+  }
+  return best;
+}
+
+}  // namespace ozgpu
+
+using namespace ozgpu;
+
+extern "C" {
+
+const char* ozgpu_last_error(void) { return g_error.c_str(); }
+const char* ozgpu_version(void) { return "ozgpu 0.1 (sm_100a, tcgen05 kind::i8)"; }
+
+int ozgpu_create(int device, ozgpu_ctx** out) {
+  return guarded([&] {
+    if (!out) throw std::invalid_argument("ozgpu_create: null output");
+    auto ctx = std::make_unique<ozgpu_ctx>();
+    init_ctx(ctx.get(), device);
+    *out = ctx.release();
+  });
+}
+
+int ozgpu_destroy(ozgpu_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+int64_t ozgpu_kernel_launches(const ozgpu_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
+
+int ozgpu_set_stage_timing(ozgpu_ctx* ctx, int enable) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("ozgpu_set_stage_timing: null context");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    ctx->timing = enable != 0;
+  });
+}
+
+int ozgpu_stage_times(ozgpu_ctx* ctx, double* ms3, int64_t* calls, int reset) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("ozgpu_stage_times: null context");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    OZ_CUDA(cudaSetDevice(ctx->device));
+    drain_events(ctx);
+    if (ms3)
+      for (int s = 0; s < 3; ++s) ms3[s] = ctx->stage_ms[s];
+    if (calls) *calls = ctx->timed_calls;
+    if (reset) {
+      ctx->stage_ms[0] = ctx->stage_ms[1] = ctx->stage_ms[2] = 0;
+      ctx->timed_calls = 0;
+    }
+  });
+}
+
+ozgpu_ctx* ozgpu_default_context(int device) {
+  if (device < 0 || device >= 64) {
+    g_error = "ozgpu_default_context: bad device index";
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lock(g_default_mu);
+  if (!g_default[device]) {
+    ozgpu_ctx* c = nullptr;
+    if (ozgpu_create(device, &c) != OZGPU_OK) return nullptr;
+    g_default[device] = c;
+  }
+  return g_default[device];
+}
+
+int ozgpu_optimal_slice_width(ozgpu_mma_config cfg, int64_t k, int* out) {
+  return guarded([&] { *out = optimal_slice_width(cfg, k); });
+}
+int ozgpu_max_inner_dim(ozgpu_mma_config cfg, int64_t* out) {
+  return guarded([&] { *out = max_inner_dim(cfg); });
+}
+int ozgpu_chi(int sa, int sb, int64_t* out) {
+  return guarded([&] { *out = chi(sa, sb); });
+}
+int ozgpu_spare_carries(int first, int last, int width, int64_t* out) {
+  return guarded([&] { *out = spare_carries(first, last, width); });
+}
+int ozgpu_plan_levels(int precision, int width, int acc_bits_used, int diagonals,
+                      ozgpu_plan* out) {
+  return guarded([&] {
+    Levels lv = plan_levels(precision, width, acc_bits_used, diagonals);
+    if (lv.levels.size() > OZGPU_MAX_LEVELS)
+      throw std::invalid_argument("plan_levels: more than 128 levels");
+    set_levels(*out, lv);
+  });
+}
+int ozgpu_diagonal_flush_threshold(ozgpu_mma_config cfg, int width, int64_t k, int64_t* out) {
+  return guarded([&] { *out = diagonal_flush_threshold(cfg, width, k); });
+}
+int ozgpu_make_plan(ozgpu_mma_config cfg, int64_t k, int sa, int sb, int schedule, int strategy,
+                    int mode, int precision, ozgpu_plan* out) {
+  return guarded([&] { *out = make_plan(cfg, k, sa, sb, schedule, strategy, mode, precision); });
+}
+
+int ozgpu_select_slices(double kappa_a, double kappa_b, int width, double u, int s_max,
+                        int has_target, double target, int schedule, int strategy,
+                        int acc_bits_used, int precision, ozgpu_selection* out) {
+  return guarded([&] {
+    try {
+      *out = select_slices(kappa_a, kappa_b, width, u, s_max, has_target != 0, target, schedule,
+                           strategy, acc_bits_used, precision);
+    } catch (const SelectionInfeasibleError& e) {
+      out->gap = e.gap;
+      out->lhs = e.best_lhs;
+      out->target = e.target;
+      throw;
+    }
+  });
+}
+
+int ozgpu_scaling_profile(ozgpu_ctx* ctx, int64_t m, int64_t k, int64_t n, const double* a,
+                          int64_t lda, const double* b, int64_t ldb, ozgpu_profile* out) {
+  return guarded([&] {
+    if (!ctx || !out) throw std::invalid_argument("scaling_profile: null argument");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    OZ_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    int64_t launches = 0;
+    double* da = static_cast<double*>(ctx->in_a.get(sizeof(double) * m * k + 8));
+    double* db = static_cast<double*>(ctx->in_b.get(sizeof(double) * k * n + 8));
+    h2d(da, a, m, k, lda, st);
+    h2d(db, b, k, n, ldb, st);
+    double* ratios = static_cast<double*>(ctx->ratios.get(sizeof(double) * (m + 1)));
+    int* zf = static_cast<int*>(ctx->status.get(sizeof(int)));
+    auto* cmax = static_cast<unsigned long long*>(ctx->colmax.get(8 * (n + 1)));
+    auto* cmin = static_cast<unsigned long long*>(ctx->colmin.get(8 * (n + 1)));
+    OZ_CUDA(cudaMemsetAsync(zf, 0, sizeof(int), st));
+    OZ_CUDA(launch_row_profile(da, k, m, k, ratios, zf, st, &launches));
+    OZ_CUDA(launch_col_profile(db, n, k, n, cmax, cmin, st, &launches));
+    std::vector<double> hr(m);
+    std::vector<unsigned long long> hmax(n), hmin(n);
+    int hz = 0;
+    if (m) OZ_CUDA(cudaMemcpyAsync(hr.data(), ratios, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
+    if (n) {
+      OZ_CUDA(cudaMemcpyAsync(hmax.data(), cmax, 8 * n, cudaMemcpyDeviceToHost, st));
+      OZ_CUDA(cudaMemcpyAsync(hmin.data(), cmin, 8 * n, cudaMemcpyDeviceToHost, st));
+    }
+    OZ_CUDA(cudaMemcpyAsync(&hz, zf, sizeof(int), cudaMemcpyDeviceToHost, st));
+    OZ_CUDA(cudaStreamSynchronize(st));
+    ctx->launches += launches;
+    double wa = 1.0, wb = 1.0;
+    for (double r : hr) wa = std::max(wa, r);
+    int bz = 0;
+    for (int64_t j = 0; j < n; ++j) {
+      if (hmax[j] == 0) {
+        bz = 1;
+        continue;
+      }
+      double mx, mn;
+      std::memcpy(&mx, &hmax[j], 8);
+      std::memcpy(&mn, &hmin[j], 8);
+      wb = std::max(wb, mx / mn);
+    }
+    out->kappa_a = 2.0 * wa;
+    out->kappa_b = 2.0 * wb;
+    out->a_has_zero_block = hz;
+    out->b_has_zero_block = bz;
+  });
+}
+
+int ozgpu_dgemm(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda,
+                const double* b, int64_t ldb, double* c, int64_t ldc, ozgpu_mma_config cfg,
+                const ozgpu_plan* plan, ozgpu_diag* diag) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("multiply: null context");
+    check_plan(plan);
+    if (m < 0 || n < 0 || k < 0) throw std::invalid_argument("multiply: shape mismatch");
+    host_multiply(ctx, m, n, k, a, lda, b, ldb, c, ldc, cfg, *plan, diag, false, 1.0, 0.0,
+                  nullptr, 0);
+  });
+}
+
+int ozgpu_dgemm_axpby(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha,
+                      const double* a, int64_t lda, const double* b, int64_t ldb, double beta,
+                      const double* c_in, int64_t ldc, double* d_out, int64_t ldd,
+                      ozgpu_mma_config cfg, const ozgpu_plan* plan, ozgpu_diag* diag) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("multiply_axpby: null context");
+    check_plan(plan);
+    if (m < 0 || n < 0 || k < 0) throw std::invalid_argument("multiply_axpby: shape mismatch");
+    host_multiply(ctx, m, n, k, a, lda, b, ldb, d_out, ldd, cfg, *plan, diag, true, alpha, beta,
+                  c_in, ldc);
+  });
+}
+
+int ozgpu_dgemm_device(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a,
+                       int64_t lda, const double* b, int64_t ldb, double* c, int64_t ldc,
+                       ozgpu_mma_config cfg, const ozgpu_plan* plan, void* stream,
+                       int* dev_status, ozgpu_diag* diag) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("multiply: null context");
+    check_plan(plan);
+    if (m < 0 || n < 0 || k < 0) throw std::invalid_argument("multiply: shape mismatch");
+    if (k < 1) throw std::invalid_argument("multiply: empty inner dimension");
+    ValidationResult v = host_validation(cfg, *plan, k);
+    if (v.capacity_error || v.precision_error) throw std::domain_error(v.message);
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    OZ_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    run_multiply(ctx, m, n, k, a, lda, b, ldb, c, ldc, cfg, *plan, st, dev_status, false, 1.0,
+                 0.0, nullptr, 0);
+    if (diag) *diag = make_diag(*plan, cfg, m, n, k, 0);
+  });
+}
+
+int ozgpu_split(ozgpu_ctx* ctx, int orientation, int64_t rows, int64_t cols, const double* x,
+                int64_t ldx, int width, int count, int mode, int64_t* slices_out,
+                int* scales_out) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("split: null context");
+    if (width < 1 || width > 62) throw std::invalid_argument("split: width out of range");
+    if (count < 1) throw std::invalid_argument("split: need at least one slice");
+    if (mode == 1 && width < 2) throw std::invalid_argument("split: nearest mode needs width >= 2");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    OZ_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    int64_t launches = 0;
+    double* dx = static_cast<double*>(ctx->in_a.get(sizeof(double) * rows * cols + 8));
+    h2d(dx, x, rows, cols, ldx, st);
+    int* status = static_cast<int*>(ctx->status.get(sizeof(int)));
+    OZ_CUDA(cudaMemsetAsync(status, 0, sizeof(int), st));
+    const int64_t blocks = orientation == 0 ? rows : cols;
+    const int64_t len = orientation == 0 ? cols : rows;
+    const int64_t kp = round_up(std::max<int64_t>(len, 1), 8);
+    int64_t* out = static_cast<int64_t*>(
+        ctx->i64o.get(sizeof(int64_t) * static_cast<size_t>(count) * blocks * kp + 8));
+    int* scales = static_cast<int*>(ctx->qa.get(sizeof(int) * (blocks + 1)));
+    if (orientation == 0) {
+      OZ_CUDA(launch_slice_rows(dx, cols, rows, cols, kp, width, count, mode, out, 1, scales,
+                                status, st, &launches));
+    } else {
+      auto* colmax = static_cast<unsigned long long*>(ctx->colmax.get(8 * (cols + 1)));
+      OZ_CUDA(launch_slice_cols(dx, cols, rows, cols, kp, width, count, mode, out, 1, scales,
+                                colmax, status, st, &launches));
+    }
+    std::vector<int64_t> host(static_cast<size_t>(count) * blocks * kp);
+    int hs = 0;
+    if (!host.empty())
+      OZ_CUDA(cudaMemcpyAsync(host.data(), out, sizeof(int64_t) * host.size(),
+                              cudaMemcpyDeviceToHost, st));
+    if (blocks)
+      OZ_CUDA(cudaMemcpyAsync(scales_out, scales, sizeof(int) * blocks, cudaMemcpyDeviceToHost, st));
+    OZ_CUDA(cudaMemcpyAsync(&hs, status, sizeof(int), cudaMemcpyDeviceToHost, st));
+    OZ_CUDA(cudaStreamSynchronize(st));
+    ctx->launches += launches;
+    if (hs & 1) throw std::invalid_argument("split: non-finite entry");
+    for (int l = 0; l < count; ++l)
+      for (int64_t bb = 0; bb < blocks; ++bb)
+        for (int64_t j = 0; j < len; ++j) {
+          int64_t v = host[(static_cast<size_t>(l) * blocks + bb) * kp + j];
+          int64_t r = orientation == 0 ? bb : j, c = orientation == 0 ? j : bb;
+          slices_out[(static_cast<size_t>(l) * rows + r) * cols + c] = v;
+        }
+  });
+}
+
+int ozgpu_integer_gemm(ozgpu_ctx* ctx, int64_t m, int64_t k, int64_t n, const int64_t* x,
+                       const int64_t* y, const int64_t* c, int64_t* out, ozgpu_mma_config cfg) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("integer_gemm: null context");
+    validate_cfg(cfg);
+    const int64_t in_lo = -(int64_t{1} << cfg.input_width), in_hi = (int64_t{1} << cfg.input_width) - 1;
+    const int64_t acc_lo = -(int64_t{1} << cfg.acc_width), acc_hi = (int64_t{1} << cfg.acc_width) - 1;
+    int64_t mx = 0, my = 0, mc = 0;
+    for (int64_t i = 0; i < m * k; ++i) {
+      if (x[i] < in_lo || x[i] > in_hi)
+        throw std::domain_error("integer_gemm: left operand entry outside I_" +
+                                std::to_string(cfg.input_width));
+      mx = std::max(mx, x[i] < 0 ? -x[i] : x[i]);
+    }
+    for (int64_t i = 0; i < k * n; ++i) {
+      if (y[i] < in_lo || y[i] > in_hi)
+        throw std::domain_error("integer_gemm: right operand entry outside I_" +
+                                std::to_string(cfg.input_width));
+      my = std::max(my, y[i] < 0 ? -y[i] : y[i]);
+    }
+    if (c)
+      for (int64_t i = 0; i < m * n; ++i) {
+        if (c[i] < acc_lo || c[i] > acc_hi)
+          throw std::domain_error("integer_gemm: accumulator input outside I_" +
+                                  std::to_string(cfg.acc_width));
+        mc = std::max(mc, c[i] < 0 ? -c[i] : c[i]);
+      }
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    OZ_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    int64_t launches = 0;
+    if (m == 0 || n == 0) return;
+    int64_t* dx = static_cast<int64_t*>(ctx->i64a.get(sizeof(int64_t) * m * k + 8));
+    int64_t* dy = static_cast<int64_t*>(ctx->i64b.get(sizeof(int64_t) * k * n + 8));
+    int64_t* dc = c ? static_cast<int64_t*>(ctx->i64c.get(sizeof(int64_t) * m * n + 8)) : nullptr;
+    int64_t* dout = static_cast<int64_t*>(ctx->i64o.get(sizeof(int64_t) * m * n + 8));
+    if (m * k) OZ_CUDA(cudaMemcpyAsync(dx, x, sizeof(int64_t) * m * k, cudaMemcpyHostToDevice, st));
+    if (k * n) OZ_CUDA(cudaMemcpyAsync(dy, y, sizeof(int64_t) * k * n, cudaMemcpyHostToDevice, st));
+    if (c) OZ_CUDA(cudaMemcpyAsync(dc, c, sizeof(int64_t) * m * n, cudaMemcpyHostToDevice, st));
+    // Tensor-core path when int8 holds the operands and no partial sum can
+    // leave I_T nor int32; otherwise the exact per-MAC checked path.
+    const __int128 bound = static_cast<__int128>(k) * mx * my + mc;
+    const bool tc = cfg.input_width <= 7 && k >= 1 && bound <= acc_hi &&
+                    bound <= static_cast<__int128>(2147483647);
+    if (tc) {
+      const int64_t kp = round_up(k, kKPad);
+      int8_t* sA = static_cast<int8_t*>(ctx->slices_a.get(static_cast<size_t>(m) * kp));
+      int8_t* sB = static_cast<int8_t*>(ctx->slices_b.get(static_cast<size_t>(n) * kp));
+      OZ_CUDA(launch_pack_i8(dx, m, k, 0, kp, sA, st, &launches));
+      OZ_CUDA(launch_pack_i8(dy, k, n, 1, kp, sB, st, &launches));
+      const int64_t ldp = round_up(n, 4);
+      int32_t* plane = static_cast<int32_t*>(ctx->planes.get(sizeof(int32_t) * m * ldp));
+      ChunkDesc one{0, 1, 1, 0, 1};
+      ChunkDesc* dch = static_cast<ChunkDesc*>(ctx->chunks.get(sizeof(ChunkDesc)));
+      OZ_CUDA(cudaMemcpyAsync(dch, &one, sizeof one, cudaMemcpyHostToDevice, st));
+      CUtensorMap tma = make_slice_map(ctx, sA, kp, m, 1, kBlockM);
+      CUtensorMap tmb = make_slice_map(ctx, sB, kp, n, 1, 256);
+      GemmArgs g{};
+      g.chunks = dch;
+      g.nchunks = 1;
+      g.m = static_cast<int>(m);
+      g.n = static_cast<int>(n);
+      g.kblocks = static_cast<int>(kp / kBlockK);
+      g.tiles_m = static_cast<int>((m + kBlockM - 1) / kBlockM);
+      g.tiles_n = static_cast<int>((n + 255) / 256);
+      g.total_units = g.tiles_m * g.tiles_n;
+      g.planes = plane;
+      g.plane_stride = m * ldp;
+      g.ldp = ldp;
+      OZ_CUDA(launch_gemm_i8(&tma, &tmb, g, ctx->num_sms, st, &launches));
+      OZ_CUDA(launch_plane_to_i64(plane, ldp, dc, dout, m, n, st, &launches));
+      OZ_CUDA(cudaMemcpyAsync(out, dout, sizeof(int64_t) * m * n, cudaMemcpyDeviceToHost, st));
+      OZ_CUDA(cudaStreamSynchronize(st));
+    } else {
+      auto* first = static_cast<unsigned long long*>(ctx->ovf.get(8));
+      OZ_CUDA(cudaMemsetAsync(first, 0xFF, 8, st));
+      OZ_CUDA(launch_integer_gemm_exact(dx, dy, dc, dout, m, k, n, cfg.acc_width, first, st,
+                                        &launches));
+      unsigned long long hf = 0;
+      OZ_CUDA(cudaMemcpyAsync(&hf, first, 8, cudaMemcpyDeviceToHost, st));
+      OZ_CUDA(cudaMemcpyAsync(out, dout, sizeof(int64_t) * m * n, cudaMemcpyDeviceToHost, st));
+      OZ_CUDA(cudaStreamSynchronize(st));
+      if (hf != ~0ULL)
+        throw OverflowError("integer accumulator overflow at (" + std::to_string(hf / n) + ", " +
+                            std::to_string(hf % n) + "): value left I_" +
+                            std::to_string(cfg.acc_width));
+    }
+    ctx->launches += launches;
+  });
+}
+
+// generators.cpp:25-49,176-182 -- std::mt19937_64 is the identical engine.
+static uint64_t splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+void ozgpu_random_uniform(int64_t m, int64_t n, uint64_t seed, double lo, double hi, double* out) {
+  std::mt19937_64 eng(splitmix64(seed));
+  const int64_t total = m * n;
+  for (int64_t i = 0; i < total; ++i)
+    out[i] = lo + static_cast<double>(eng() >> 11) * 0x1p-53 * (hi - lo);
+}
+
+void ozgpu_gen_kappa_d(int64_t n, double kappa_d, uint64_t seed, int rotate, double* a,
+                       double* b) {
+  std::mt19937_64 ea(splitmix64(seed + 1)), eb(splitmix64(seed + 2));
+  for (int64_t i = 0; i < n * n; ++i) a[i] = 1.0 + static_cast<double>(ea() >> 11) * 0x1p-53 * 1.0;
+  for (int64_t i = 0; i < n * n; ++i) b[i] = 1.0 + static_cast<double>(eb() >> 11) * 0x1p-53 * 1.0;
+  std::vector<double> d(n);
+  double log_kd = std::log(kappa_d);
+  for (int64_t i = 0; i < n; ++i) {
+    double frac = n > 1 ? static_cast<double>(i) / static_cast<double>(n - 1) : 0.5;
+    d[i] = std::exp(log_kd * (frac - 0.5));
+  }
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      a[i * n + j] *= d[j];
+      b[i * n + j] /= d[i];
+    }
+  if (rotate) {
+    std::vector<double> ra(n * n), rb(n * n);
+    for (int64_t i = 0; i < n; ++i) {
+      int64_t shift = (i + 1) % n;
+      for (int64_t j = 0; j < n; ++j) {
+        ra[i * n + (j + shift) % n] = a[i * n + j];
+        rb[((j + shift) % n) * n + i] = b[j * n + i];
+      }
+    }
+    std::memcpy(a, ra.data(), sizeof(double) * n * n);
+    std::memcpy(b, rb.data(), sizeof(double) * n * n);
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,95 @@
+// Internal interface between the host orchestration (ozgpu_host.cpp) and
+// the sm_100a kernels (ozgpu_kernels.cu).  Not installed; not part of the ABI.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ozgpu {
+
+// GEMM tile geometry (tcgen05 kind::i8, one CTA per 128-row tile).
+constexpr int kBlockM = 128;
+constexpr int kBlockK = 128;  // bytes of K per pipeline stage (= 4 MMAs of K=32)
+constexpr int kKPad = 128;    // slice rows are padded to a multiple of this
+
+// One accumulation chunk: consecutive pairs (l0 + p, d + 2 - l0 - p),
+// p in [0, npairs), all on diagonal d (shared scale 2^w(d)).  The exact
+// combine adds the chunk's int32 sum shifted left by `shift` bits, with
+// shift = (D - 1 - d) * t, so that the least significant diagonal has
+// weight 2^0 (scheme.cpp:252-262).
+struct ChunkDesc {
+  int d;
+  int l0;
+  int npairs;
+  int shift;
+  int flush;  // sequential strategies: 1 = a reference chunk ends here (scheme.cpp:281-313)
+};
+
+struct GemmArgs {
+  const ChunkDesc* chunks;
+  int nchunks;
+  int m, n;
+  int kblocks;        // kp / kBlockK
+  int tiles_m, tiles_n;
+  int total_units;    // tiles_m * tiles_n * nchunks (split mode)
+  int32_t* planes;    // [nchunks][m][ldp] int32 chunk sums
+  int64_t plane_stride;
+  int64_t ldp;
+};
+
+struct CombineArgs {
+  const int32_t* planes;
+  const ChunkDesc* chunks;
+  int nchunks;
+  int64_t plane_stride;
+  int64_t ldp;
+  const int* qa;
+  const int* qb;
+  int m, n;
+  long w_last;         // exponent of the least significant diagonal: -(D+1)t (+2 nearest)
+  int width;           // t
+  int diagonals;       // D
+  int mode;            // 0 truncate, 1 nearest
+  double* c;
+  int64_t ldc;
+  int* realized_psi;   // device int (atomicMax), sequential strategies only
+  // optional axpby epilogue (scheme.cpp:363-372): d = alpha*c + beta*cin
+  int axpby;
+  double alpha, beta;
+  const double* cin;
+  int64_t ldcin;
+};
+
+// Launchers (return cudaError_t; 0 == success).  `launches` counts kernels.
+cudaError_t launch_slice_rows(const double* a, int64_t lda, int64_t m, int64_t k, int64_t kp,
+                              int width, int count, int mode, void* out, int out_is_i64,
+                              int* scales, int* status, cudaStream_t st, int64_t* launches);
+cudaError_t launch_slice_cols(const double* b, int64_t ldb, int64_t k, int64_t n, int64_t kp,
+                              int width, int count, int mode, void* out, int out_is_i64,
+                              int* scales, unsigned long long* colmax, int* status,
+                              cudaStream_t st, int64_t* launches);
+cudaError_t launch_gemm_i8(const CUtensorMap* tma, const CUtensorMap* tmb, const GemmArgs& args,
+                           int num_sms, cudaStream_t st, int64_t* launches);
+int gemm_smem_bytes();
+cudaError_t launch_combine_exact(const CombineArgs& args, int words, cudaStream_t st,
+                                 int64_t* launches);
+cudaError_t launch_combine_sequential(const CombineArgs& args, cudaStream_t st,
+                                      int64_t* launches);
+cudaError_t launch_row_profile(const double* a, int64_t lda, int64_t m, int64_t k,
+                               double* ratios, int* zero_flag, cudaStream_t st,
+                               int64_t* launches);
+cudaError_t launch_col_profile(const double* b, int64_t ldb, int64_t k, int64_t n,
+                               unsigned long long* colmax, unsigned long long* colmin,
+                               cudaStream_t st, int64_t* launches);
+cudaError_t launch_pack_i8(const int64_t* x, int64_t rows, int64_t cols, int transpose,
+                           int64_t kp, int8_t* out, cudaStream_t st, int64_t* launches);
+cudaError_t launch_integer_gemm_exact(const int64_t* x, const int64_t* y, const int64_t* c,
+                                      int64_t* out, int64_t m, int64_t k, int64_t n,
+                                      int acc_width, unsigned long long* first_overflow,
+                                      cudaStream_t st, int64_t* launches);
+cudaError_t launch_plane_to_i64(const int32_t* plane, int64_t ldp, const int64_t* c,
+                                int64_t* out, int64_t m, int64_t n, cudaStream_t st,
+                                int64_t* launches);
+
+}  // namespace ozgpu

@@ -1,0 +1,32 @@
+"""Shared input builders (mirroring the reference tests' fixed-seed builders,
+e.g. proj/tests/scheme_test.cpp:44-54)."""
+import numpy as np
+
+
+def random_matrix(rows, cols, rng, exp_lo=-4, exp_hi=4, zero_frac=0.0):
+    """(1 + frac) * 2^e * sign with e uniform in [exp_lo, exp_hi]."""
+    frac = rng.integers(0, 2**53, size=(rows, cols), dtype=np.int64).astype(np.float64) * 2.0**-53
+    e = rng.integers(exp_lo, exp_hi + 1, size=(rows, cols))
+    sign = np.where(rng.integers(0, 2, size=(rows, cols)) == 1, 1.0, -1.0)
+    out = np.ldexp(1.0 + frac, e) * sign
+    if zero_frac:
+        out[rng.random((rows, cols)) < zero_frac] = 0.0
+    return out
+
+
+def uniform(rows, cols, rng, lo=-0.5, hi=0.5):
+    return lo + rng.random((rows, cols)) * (hi - lo)
+
+
+def bits_equal(x, y) -> bool:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    return x.shape == y.shape and np.array_equal(x.view(np.uint64), y.view(np.uint64))
+
+
+def mismatch_report(x, y, limit=5) -> str:
+    x = np.asarray(x)
+    y = np.asarray(y)
+    bad = np.argwhere(x.view(np.uint64) != y.view(np.uint64))
+    rows = [f"{tuple(i)}: got {x[tuple(i)]!r} want {y[tuple(i)]!r}" for i in bad[:limit]]
+    return f"{len(bad)} mismatches; " + "; ".join(rows)

@@ -1,0 +1,232 @@
+"""GPU parity: the CUDA path through the C-ABI against the compiled reference
+(oracle/_ref) and the C restatement, bit-exact (slices, pair products, the
+levelled-exact C, and the sequential strategies in matched order)."""
+import itertools
+
+import numpy as np
+import pytest
+
+from helpers import bits_equal, mismatch_report, random_matrix, uniform
+
+pytestmark = pytest.mark.gpu
+
+STRATS = (0, 1, 2)
+
+
+def _diag_tuple(d):
+    return (d.products, d.integer_adds, d.float_adds, d.flushes, d.realized_psi, d.planned_psi,
+            d.width, d.acc_bits_used)
+
+
+# ---------------------------------------------------------------- slicing
+
+@pytest.mark.parametrize("shape", [(1, 1), (3, 5), (17, 130), (64, 257), (9, 1000)])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_split_matches_reference(oz, ref, shape, mode):
+    rng = np.random.default_rng(hash((shape, mode)) % 2**32)
+    for exps, zf in [((-4, 4), 0.0), ((-40, 40), 0.1), ((-1074, -1000), 0.0), ((1000, 1023), 0.2)]:
+        x = random_matrix(*shape, rng, *exps, zero_frac=zf)
+        for width, count in [(7, 4), (7, 9), (3, 5), (5, 17), (2, 3)]:
+            sa = oz.split_rows(x, width, count, oz.SliceMode(mode))
+            wsc, wsl = ref.ref_split(x, 0, width, count, mode)
+            assert np.array_equal(sa.scale_exponents, wsc)
+            assert np.array_equal(sa.slices, wsl), (exps, width, count)
+            sb = oz.split_cols(x, width, count, oz.SliceMode(mode))
+            wsc, wsl = ref.ref_split(x, 1, width, count, mode)
+            assert np.array_equal(sb.scale_exponents, wsc)
+            assert np.array_equal(sb.slices, wsl), (exps, width, count)
+
+
+def test_split_wide_widths_and_errors(oz, ref):
+    rng = np.random.default_rng(5)
+    x = random_matrix(7, 11, rng, -30, 30, zero_frac=0.1)
+    for width, count in [(20, 3), (62, 2), (11, 6)]:
+        for mode in (0, 1):
+            s = oz.split_rows(x, width, count, oz.SliceMode(mode))
+            wsc, wsl = ref.ref_split(x, 0, width, count, mode)
+            assert np.array_equal(s.slices, wsl) and np.array_equal(s.scale_exponents, wsc)
+    bad = x.copy()
+    bad[2, 3] = np.inf
+    with pytest.raises(oz.InvalidArgument):
+        oz.split_rows(bad, 7, 2)
+    negz = x.copy()
+    negz[0, 0] = -0.0  # split accepts negative zeros (only multiply rejects them)
+    s = oz.split_rows(negz, 7, 2)
+    assert s.slices[:, 0, 0].tolist() == [0, 0]
+    with pytest.raises(oz.InvalidArgument):
+        oz.split_rows(x, 0, 2)
+    with pytest.raises(oz.InvalidArgument):
+        oz.split_rows(x, 7, 0)
+
+
+def test_golden_worked_example_slices(oz):
+    # proj/tests/slicing_test.cpp:73-99, acceptance_test.cpp:64-100
+    a = np.array([[1.5625, 8.0, -3.6875]])
+    b = np.array([[1.3828125], [-7.625], [3.625]])
+    sa = oz.split_rows(a, 3, 4)
+    sb = oz.split_cols(b, 3, 4)
+    assert sa.scale_exponents.tolist() == [4] and sb.scale_exponents.tolist() == [3]
+    assert sa.slices[:, 0, :].tolist() == [[0, 4, -1], [6, 0, -6], [2, 0, -6], [0, 0, 0]]
+    assert sb.slices[:, :, 0].tolist() == [[1, -7, 3], [3, -5, 5], [0, 0, 0], [4, 0, 0]]
+    cfg = oz.MmaConfig(3, 31)
+    want = {(1, 1): -31, (1, 2): -25, (2, 1): -12, (1, 3): 0, (2, 2): -12, (3, 1): -16,
+            (1, 4): 0, (2, 3): 0, (3, 2): -24, (4, 1): 0}
+    for (l, h), v in want.items():
+        e = oz.integer_gemm(sa.slices[l - 1], sb.slices[h - 1], cfg)
+        assert e[0, 0] == v
+    full = oz.make_plan(cfg, 3, 4, 4, oz.ScheduleKind.FULL)
+    assert oz.multiply(a, b, cfg, full).c[0, 0] == -72.20654296875
+    red = oz.make_plan(cfg, 3, 4, 4, oz.ScheduleKind.REDUCED)
+    r = oz.multiply(a, b, cfg, red)
+    assert r.c[0, 0] == -72.21875
+    assert r.diagnostics.products == oz.chi(4, 4)
+
+
+# --------------------------------------------------------- pair products
+
+@pytest.mark.parametrize("mkn", [(1, 1, 1), (5, 3, 7), (128, 128, 256), (130, 300, 257),
+                                 (257, 1024, 129)])
+def test_integer_gemm_tensor_path(oz, ref, mkn):
+    m, k, n = mkn
+    rng = np.random.default_rng(m * 1000 + n)
+    x = rng.integers(-128, 128, size=(m, k))
+    y = rng.integers(-128, 128, size=(k, n))
+    cfg = oz.MmaConfig.int8_int32()
+    got = oz.integer_gemm(x, y, cfg)
+    assert np.array_equal(got, ref.ref_integer_gemm(x, y))
+    c = rng.integers(-1000, 1000, size=(m, n))
+    got_c = oz.integer_gemm(x, y, cfg, c)
+    assert np.array_equal(got_c, ref.ref_integer_gemm(x, y) + c)
+
+
+def test_integer_gemm_overflow_matches_reference(oz, ref):
+    rng = np.random.default_rng(3)
+    x = rng.integers(120, 128, size=(4, 64))
+    y = rng.integers(120, 128, size=(64, 5))
+    cfg = oz.MmaConfig(7, 19)  # 64 * 127^2 exceeds I_19
+    with pytest.raises(ref.RefError) as want:
+        ref.ref_integer_gemm(x, y, 7, 19)
+    assert want.value.code == 5
+    with pytest.raises(oz.MmaOverflowError) as got:
+        oz.integer_gemm(x, y, cfg)
+    assert str(got.value) == want.value.msg
+    with pytest.raises(oz.DomainError):
+        oz.integer_gemm(np.full((2, 2), 200), y[:2], cfg)
+
+
+# ---------------------------------------------------------------- multiply
+
+SHAPES = [(1, 1, 1), (5, 7, 3), (33, 100, 17), (129, 257, 130), (200, 64, 300)]
+
+
+@pytest.mark.parametrize("mkn", SHAPES)
+def test_multiply_levelled_matches_reference(oz, ref, mkn):
+    m, k, n = mkn
+    rng = np.random.default_rng(sum(mkn))
+    cfg = oz.MmaConfig.int8_int32()
+    inputs = [(uniform(m, k, rng), uniform(k, n, rng)),
+              (random_matrix(m, k, rng, -20, 20, 0.05), random_matrix(k, n, rng, -20, 20, 0.05))]
+    for (a, b), (sa, sb), sched, mode in itertools.product(
+            inputs, [(1, 1), (4, 4), (3, 7), (8, 8), (13, 12)], (0, 1), (0, 1)):
+        plan = oz.make_plan(cfg, k, sa, sb, oz.ScheduleKind(sched), oz.Accumulation(2),
+                            oz.SliceMode(mode))
+        got = oz.multiply(a, b, cfg, plan)
+        want, wd = ref.ref_multiply(a, b, sa, sb, sched, 2, mode)
+        assert bits_equal(got.c, want), (sa, sb, sched, mode, mismatch_report(got.c, want))
+        assert _diag_tuple(got.diagnostics) == tuple(wd.tolist())
+
+
+@pytest.mark.parametrize("strategy", [0, 1])
+def test_multiply_sequential_strategies_match_reference(oz, ref, strategy):
+    rng = np.random.default_rng(40 + strategy)
+    cfg = oz.MmaConfig.int8_int32()
+    for (m, k, n) in [(6, 9, 5), (64, 300, 70), (130, 129, 33)]:
+        a = random_matrix(m, k, rng, -12, 12, 0.05)
+        b = random_matrix(k, n, rng, -12, 12, 0.05)
+        for (sa, sb), sched, mode in itertools.product([(3, 3), (6, 6), (5, 9)], (0, 1), (0, 1)):
+            plan = oz.make_plan(cfg, k, sa, sb, oz.ScheduleKind(sched),
+                                oz.Accumulation(strategy), oz.SliceMode(mode))
+            got = oz.multiply(a, b, cfg, plan)
+            want, wd = ref.ref_multiply(a, b, sa, sb, sched, strategy, mode)
+            assert bits_equal(got.c, want), (m, k, n, sa, sb, sched, mode,
+                                              mismatch_report(got.c, want))
+            assert _diag_tuple(got.diagnostics) == tuple(wd.tolist())
+
+
+def test_multiply_error_free_at_exact_slice_counts(oz, ref):
+    # acceptance criterion 2 (acceptance_test.cpp:105-133), fewer seeds
+    rng = np.random.default_rng(20250809)
+    cfg = oz.MmaConfig.int8_int32()
+    for _ in range(25):
+        m, k, n = (int(v) for v in rng.integers(1, 33, size=3))
+        a = random_matrix(m, k, rng, -40, 40)
+        b = random_matrix(k, n, rng, -40, 40)
+        t = oz.optimal_slice_width(cfg, k)
+        sa = ref.ref_min_exact_slices(a, 0, t)
+        sb = ref.ref_min_exact_slices(b, 1, t)
+        plan = oz.make_plan(cfg, k, sa, sb, oz.ScheduleKind.FULL)
+        got = oz.multiply(a, b, cfg, plan).c
+        assert bits_equal(got, ref.ref_exact_gemm(a, b))
+
+
+def test_multiply_input_errors(oz):
+    cfg = oz.MmaConfig.int8_int32()
+    a = np.ones((1, 2))
+    b = np.ones((2, 1))
+    plan = oz.make_plan(cfg, 2, 1, 1)
+    for bad in (np.inf, np.nan, -0.0):
+        aa = a.copy()
+        aa[0, 1 if bad != -0.0 else 0] = bad
+        with pytest.raises(oz.InvalidArgument):
+            oz.multiply(aa, b, cfg, plan)
+    forged = oz.make_plan(cfg, 2, 2, 2)
+    forged.width = 16  # scheme_test.cpp:294-302
+    with pytest.raises(oz.DomainError, match="65536"):
+        oz.multiply(a, b, cfg, forged)
+    with pytest.raises(oz.InvalidArgument):
+        oz.multiply(np.ones((1, 0)), np.ones((0, 1)), cfg, plan)
+    with pytest.raises(oz.InvalidArgument):
+        oz.multiply(np.ones((2, 3)), np.ones((2, 3)), cfg, plan)
+
+
+def test_multiply_axpby_matches_reference(oz, ref):
+    rng = np.random.default_rng(21)
+    cfg = oz.MmaConfig.int8_int32()
+    a = random_matrix(40, 60, rng)
+    b = random_matrix(60, 50, rng)
+    c = random_matrix(40, 50, rng)
+    for sa, sb, sched in [(4, 4, 0), (8, 8, 1)]:
+        plan = oz.make_plan(cfg, 60, sa, sb, oz.ScheduleKind(sched))
+        got = oz.multiply_axpby(-2.5, a, b, 0.5, c, cfg, plan).c
+        want = ref.ref_multiply_axpby(-2.5, a, b, 0.5, c, sa, sb, sched)
+        assert bits_equal(got, want)
+
+
+def test_scaling_profile_matches_reference(oz, ref):
+    rng = np.random.default_rng(9)
+    a = random_matrix(50, 70, rng, -30, 30, 0.1)
+    b = random_matrix(70, 40, rng, -30, 30, 0.1)
+    a[3, :] = 0.0
+    p = oz.scaling_profile(a, b)
+    assert (p.kappa_a, p.kappa_b, p.a_has_zero_block, p.b_has_zero_block) == \
+        ref.ref_scaling_profile(a, b)
+
+
+def test_badly_scaled_kappa_d(oz, ref):
+    # acceptance criterion 8 style: gen_kappa_d with rotation, bit-exact C
+    a, b = oz.gen_kappa_d(96, 2.0**60, 7, True)
+    wa, wb = ref.ref_gen_kappa_d(96, 2.0**60, 7, True)
+    assert bits_equal(a, wa) and bits_equal(b, wb)
+    cfg = oz.MmaConfig.int8_int32()
+    for sa, sb in [(8, 8), (16, 17)]:
+        plan = oz.make_plan(cfg, 96, sa, sb)
+        got = oz.multiply(a, b, cfg, plan).c
+        want, _ = ref.ref_multiply(a, b, sa, sb)
+        assert bits_equal(got, want), mismatch_report(got, want)
+
+
+def test_native_kernels_launched(oz):
+    cfg = oz.MmaConfig.int8_int32()
+    before = oz.kernel_launches()
+    oz.multiply(np.ones((8, 8)), np.ones((8, 8)), cfg, oz.make_plan(cfg, 8, 2, 2))
+    assert oz.kernel_launches() - before >= 4
