@@ -269,6 +269,8 @@ def main():
     blk = shard.block_of(rank, world, pr * m, pc * n)
     mcfg = oz.MmaConfig.int8_int32()
     dev = torch.device(f"cuda:{local}")
+    # a dedicated stream: CUDA events and the library's kernels share it
+    torch.cuda.set_stream(torch.cuda.Stream(device=dev))
 
     # inputs: A row-panel i on rank (i, 0), B column-panel j on rank (0, j)
     a_h, b_h = make_inputs(oz, cfg, blk.i, blk.j)
@@ -427,6 +429,8 @@ def main():
                 bs = 64
                 blocks = cpu_blocks(m, n, threads, bs)
                 c_ref, secs = run_cpu_reference(a_h, b_h, slices, blocks, threads)
+                step(plan)  # C of the headline plan (the sweep overwrote c_d)
+                torch.cuda.synchronize()
                 c_gpu = c_d.cpu().numpy()
                 same = all(np.array_equal(c_ref[r0:r1, c0:c1].view(np.uint64),
                                           c_gpu[r0:r1, c0:c1].view(np.uint64))

@@ -164,9 +164,9 @@ int ozgpu_dgemm_axpby(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, double al
                       const double* c_in, int64_t ldc, double* d_out, int64_t ldd,
                       ozgpu_mma_config cfg, const ozgpu_plan* plan, ozgpu_diag* diag);
 /* Device-resident twin: a, b, c are device pointers; the work is enqueued on
- * `stream` (0 = the context stream) and the call returns without
+ * `stream` (a cudaStream_t; NULL is the legacy default stream) and the call returns without
  * synchronising.  Input validity (Inf/NaN/-0, scheme.cpp:223-225) is
- * reported through *dev_status (device int, may be NULL): 0 ok, 1 dirty. */
+ * reported through *dev_status (device int, may be NULL): 0 ok, nonzero dirty. */
 int ozgpu_dgemm_device(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a,
                        int64_t lda, const double* b, int64_t ldb, double* c, int64_t ldc,
                        ozgpu_mma_config cfg, const ozgpu_plan* plan, void* stream,

@@ -1,0 +1,318 @@
+// tcgen05 kind::i8 pair GEMMs of the B200-native Ozaki-I FP64 GEMM
+// (replaces integer_gemm, proj/src/mma_sim.cpp:76-114, and the levelled
+// accumulation, proj/src/scheme.cpp:314-355).
+//
+// Persistent, warp-specialised, one 128 x 256 output tile per work unit:
+//   warp 0      TMA producer (3-D tensor maps over the [slice][row][kp] int8
+//               slices, 128-byte swizzle, 4-stage mbarrier ring)
+//   warp 1      MMA issuer: one thread issues tcgen05.mma.cta_group::1.kind::i8
+//               (M=128, N=256, K=32) into a double-buffered int32 TMEM
+//               accumulator (2 x 256 columns)
+//   warp 2      TMEM allocator
+//   warps 4..7  epilogue (TMEM lane quadrant = warp % 4)
+//
+// A "chunk" is a run of pairs on one diagonal whose int32 sum cannot
+// overflow; its K loop runs over the concatenated slices (pairs x kp).
+//
+// Two epilogue modes:
+//   split  (W == 0)  unit = (tile, chunk); the int32 chunk sum is written to
+//                    plane[chunk] and a separate combine kernel rounds.
+//   fused  (W = 2,3) unit = tile; the CTA walks every chunk of the tile and
+//                    the epilogue folds each chunk sum, shifted by its
+//                    diagonal weight, into a W-word exact integer per element
+//                    kept in a CTA-private scratch (L2-resident); after the
+//                    last chunk it rounds once (ExactValue::to_double,
+//                    oracle.cpp:157-180) and stores C through an XOR-swizzled
+//                    smem transpose so each warp writes whole rows.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ozgpu_internal.h"
+#include "ozgpu_numeric.h"
+#include "ozgpu_ptx.cuh"
+
+namespace ozgpu {
+
+constexpr int kBN = 256;
+constexpr int kStages = 4;
+constexpr int kABytes = kBlockM * kBlockK;  // 16 KB
+constexpr int kBBytes = kBN * kBlockK;      // 32 KB
+constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kTmemCols = 2 * kBN;  // double-buffered accumulator
+constexpr int kGemmThreads = 256;
+constexpr int kStagingBytes = 4 * 32 * 32 * 8;  // fused epilogue: 32x32 f64 per warp
+constexpr int kSmemSplit = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kSmemFused = kSmemSplit + kStagingBytes;
+
+int gemm_smem_bytes() { return kSmemFused; }
+
+struct TileCoord {
+  int tm, tn;
+};
+
+// Grouped rasterisation: consecutive tiles walk 8 tile-rows at a time so
+// concurrently running CTAs share A and B slice panels in L2.
+__device__ __forceinline__ TileCoord decode_tile(int t, const GemmArgs& p) {
+  const int G = 8;
+  const int group_size = G * p.tiles_n;
+  const int group = t / group_size;
+  const int first_m = group * G;
+  const int gsz = p.tiles_m - first_m < G ? p.tiles_m - first_m : G;
+  const int in_group = t - group * group_size;
+  TileCoord c;
+  c.tm = first_m + in_group % gsz;
+  c.tn = in_group / gsz;
+  return c;
+}
+
+// Work unit -> (tile, first chunk, chunk count).
+__device__ __forceinline__ void decode_unit(int unit, const GemmArgs& p, bool fused,
+                                            TileCoord& tc, int& c0, int& nc) {
+  if (fused) {
+    tc = decode_tile(unit, p);
+    c0 = 0;
+    nc = p.nchunks;
+  } else {
+    const int tiles = p.tiles_m * p.tiles_n;
+    c0 = unit / tiles;
+    nc = 1;
+    tc = decode_tile(unit - c0 * tiles, p);
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_i8_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
+                   const GemmArgs p) {
+  constexpr bool kFused = W > 0;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kStages * kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  double* staging = reinterpret_cast<double*>(smem + kStages * kStageBytes + 256);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmb)) : "memory");
+  }
+  if (warp == 2) tmem_alloc(tmem_holder, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer ----------------
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int unit = blockIdx.x; unit < p.total_units; unit += gridDim.x) {
+      TileCoord tc;
+      int c0, nc;
+      decode_unit(unit, p, kFused, tc, c0, nc);
+      for (int c = c0; c < c0 + nc; ++c) {
+        const ChunkDesc cd = p.chunks[c];
+        for (int pr = 0; pr < cd.npairs; ++pr) {
+          const int l = cd.l0 + pr;
+          const int h = cd.d + 2 - l;
+          for (int kb = 0; kb < p.kblocks; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], kStageBytes);
+            tma_load_3d(sA + stage * kABytes, &tma, &full[stage], kb * kBlockK, tc.tm * kBlockM,
+                        l - 1);
+            tma_load_3d(sB + stage * kBBytes, &tmb, &full[stage], kb * kBlockK, tc.tn * kBN,
+                        h - 1);
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer (single thread) ----------------
+    constexpr uint32_t idesc = idesc_i8<kBlockM, kBN>();
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int unit = blockIdx.x; unit < p.total_units; unit += gridDim.x) {
+      TileCoord tc;
+      int c0, nc;
+      decode_unit(unit, p, kFused, tc, c0, nc);
+      for (int c = c0; c < c0 + nc; ++c, ++it) {
+        const ChunkDesc cd = p.chunks[c];
+        const int acc = it & 1;
+        const uint32_t aphase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * kBN;
+        const int total = cd.npairs * p.kblocks;
+        for (int i = 0; i < total; ++i) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t ad = sdesc_sw128(smem_addr(sA + stage * kABytes));
+          const uint64_t bd = sdesc_sw128(smem_addr(sB + stage * kBBytes));
+#pragma unroll
+          for (int kk = 0; kk < kBlockK / 32; ++kk)
+            tc_mma_i8(tmem_d, ad + 2 * kk, bd + 2 * kk, idesc, (i | kk) != 0);
+          tc_commit(&empty[stage]);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue ----------------
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    double* stage_w = staging + q * 32 * 32;
+    uint64_t* scratch = nullptr;
+    if constexpr (kFused)
+      scratch = p.scratch + static_cast<size_t>(blockIdx.x) * W * kBN * kBlockM;
+    int it = 0;
+    for (int unit = blockIdx.x; unit < p.total_units; unit += gridDim.x) {
+      TileCoord tc;
+      int c0, nc;
+      decode_unit(unit, p, kFused, tc, c0, nc);
+      const int row0 = tc.tm * kBlockM + q * 32;
+      const int row = row0 + lane;
+      long qrow = 0;
+      if constexpr (kFused) qrow = row < p.m ? __ldg(p.qa + row) : 0;
+      for (int c = c0; c < c0 + nc; ++c, ++it) {
+        const int acc = it & 1;
+        const uint32_t aphase = (it >> 1) & 1;
+        mbar_wait(&tfull[acc], aphase);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * kBN;
+        if constexpr (!kFused) {
+          int32_t* dst = p.planes + static_cast<int64_t>(c) * p.plane_stride +
+                         static_cast<int64_t>(row) * p.ldp;
+#pragma unroll 1
+          for (int s0 = 0; s0 < kBN; s0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(taddr + s0, r);
+            const int col0 = tc.tn * kBN + s0;
+            if (row < p.m) {
+              if (col0 + 32 <= p.n && (p.ldp & 3) == 0) {
+                int4* d4 = reinterpret_cast<int4*>(dst + col0);
+#pragma unroll
+                for (int v = 0; v < 8; ++v)
+                  d4[v] = make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+              } else {
+                for (int v = 0; v < 32; ++v)
+                  if (col0 + v < p.n) dst[col0 + v] = static_cast<int32_t>(r[v]);
+              }
+            }
+          }
+        } else {
+          const bool first = c == 0, last = c == p.nchunks - 1;
+          const int shift = p.chunks[c].shift;
+#pragma unroll 1
+          for (int s0 = 0; s0 < kBN; s0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(taddr + s0, r);
+            // scratch layout [word][column][row]: a warp touches 256 contiguous bytes
+            uint64_t* sp = scratch + static_cast<size_t>(s0) * kBlockM + q * 32 + lane;
+            const int col0 = tc.tn * kBN + s0;
+            int qcol = 0;
+            if (last) qcol = col0 + lane < p.n ? __ldg(p.qb + col0 + lane) : 0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              uint64_t v[W];
+#pragma unroll
+              for (int w = 0; w < W; ++w)
+                v[w] = first ? 0ULL : sp[(static_cast<size_t>(w) * kBN + j) * kBlockM];
+              words_add_shifted<W>(v, static_cast<int32_t>(r[j]), shift);
+              const int qj = __shfl_sync(0xFFFFFFFFu, qcol, j);
+              if (!last) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) sp[(static_cast<size_t>(w) * kBN + j) * kBlockM] = v[w];
+              } else {
+                const double d = round_words<W>(v, qrow + qj + p.w_last);
+                stage_w[lane * 32 + (j ^ lane)] = d;
+              }
+            }
+            if (last) {
+              __syncwarp();
+              const int col = col0 + lane;
+#pragma unroll 4
+              for (int rr = 0; rr < 32; ++rr) {
+                const int orow = row0 + rr;
+                double d = stage_w[rr * 32 + (lane ^ rr)];
+                if (orow < p.m && col < p.n) {
+                  if (p.axpby)
+                    d = __dadd_rn(__dmul_rn(p.alpha, d),
+                                  __dmul_rn(p.beta, p.cin[static_cast<int64_t>(orow) * p.ldcin + col]));
+                  p.c[static_cast<int64_t>(orow) * p.ldc + col] = d;
+                }
+              }
+              __syncwarp();
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, kTmemCols);
+  }
+}
+
+template <int W>
+static cudaError_t launch_t(const CUtensorMap* tma, const CUtensorMap* tmb, const GemmArgs& args,
+                            int grid, int smem, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(gemm_i8_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  gemm_i8_kernel<W><<<grid, kGemmThreads, smem, st>>>(*tma, *tmb, args);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gemm_i8(const CUtensorMap* tma, const CUtensorMap* tmb, const GemmArgs& args,
+                           int num_sms, cudaStream_t st, int64_t* launches) {
+  const int grid = args.total_units < num_sms ? args.total_units : num_sms;
+  if (grid < 1) return cudaSuccess;
+  cudaError_t e;
+  switch (args.fused_words) {
+    case 0: e = launch_t<0>(tma, tmb, args, grid, kSmemSplit, st); break;
+    case 2: e = launch_t<2>(tma, tmb, args, grid, kSmemFused, st); break;
+    case 3: e = launch_t<3>(tma, tmb, args, grid, kSmemFused, st); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (e == cudaSuccess) ++*launches;
+  return e;
+}
+
+}  // namespace ozgpu

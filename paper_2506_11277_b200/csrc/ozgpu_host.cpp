@@ -12,6 +12,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -106,7 +107,7 @@ struct ozgpu_ctx {
   std::atomic<int64_t> launches{0};
   ozgpu::EncodeTiledFn encode = nullptr;
   // workspace
-  ozgpu::DevBuf slices_a, slices_b, qa, qb, colmax, colmin, status, planes, chunks, psi;
+  ozgpu::DevBuf slices_a, slices_b, qa, qb, colmax, colmin, status, planes, chunks, psi, scratch;
   ozgpu::DevBuf in_a, in_b, io_c, in_c2, ratios, i64a, i64b, i64c, i64o, ovf;
   std::vector<ozgpu::ChunkDesc> host_chunks;
   // stage timing (ozgpu_set_stage_timing)
@@ -366,15 +367,37 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
 
   int* psi_dev = nullptr;
   if (m > 0 && n > 0 && !cp.chunks.empty()) {
-    const int64_t ldp = round_up(n, 4);
-    const int64_t plane = m * ldp;
-    int32_t* planes = static_cast<int32_t*>(
-        ctx->planes.get(sizeof(int32_t) * static_cast<size_t>(plane) * cp.chunks.size()));
+    const int tiles_m = static_cast<int>((m + kBlockM - 1) / kBlockM);
+    const int tiles_n = static_cast<int>((n + 255) / 256);
+    const int64_t tiles = static_cast<int64_t>(tiles_m) * tiles_n;
+    const long w_last = -static_cast<long>(cp.diagonals + 1) * t + (p.mode == 1 ? 2 : 0);
+    // Fused exact epilogue when the tiles alone fill the GPU and the exact
+    // value fits 2-3 words; otherwise (small problems, sequential strategies,
+    // very wide exact values) split units over (tile, chunk) + combine kernel.
+    int words = p.strategy == 2 ? exact_words(cp.diagonals, t, cp.chunks.size()) : 0;
+    bool fused = p.strategy == 2 && words <= 3 && tiles >= ctx->num_sms;
+    if (const char* env = std::getenv("OZGPU_EPILOGUE")) {
+      if (std::string(env) == "split") fused = false;
+      if (std::string(env) == "fused" && p.strategy == 2 && words <= 3) fused = true;
+    }
+    if (fused) {
+      if (words < 2) words = 2;
+      // Alternate long and short chunks so the epilogue of a short chunk
+      // overlaps the MMAs of a long one (the exact sum is order-free).
+      std::vector<ChunkDesc> sorted = cp.chunks;
+      std::stable_sort(sorted.begin(), sorted.end(),
+                       [](const ChunkDesc& x, const ChunkDesc& y) { return x.npairs > y.npairs; });
+      std::vector<ChunkDesc> order;
+      for (size_t lo = 0, hi = sorted.size(); lo < hi;) {
+        order.push_back(sorted[lo++]);
+        if (lo < hi) order.push_back(sorted[--hi]);
+      }
+      cp.chunks = order;
+    }
     ChunkDesc* dchunks =
         static_cast<ChunkDesc*>(ctx->chunks.get(sizeof(ChunkDesc) * cp.chunks.size()));
     OZ_CUDA(cudaMemcpyAsync(dchunks, cp.chunks.data(), sizeof(ChunkDesc) * cp.chunks.size(),
                             cudaMemcpyHostToDevice, st));
-    // keep the host copy alive until the stream consumes it
     ctx->host_chunks = cp.chunks;
 
     CUtensorMap tma = make_slice_map(ctx, slA, kp, m, sa, kBlockM);
@@ -385,9 +408,38 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
     g.m = static_cast<int>(m);
     g.n = static_cast<int>(n);
     g.kblocks = static_cast<int>(kp / kBlockK);
-    g.tiles_m = static_cast<int>((m + kBlockM - 1) / kBlockM);
-    g.tiles_n = static_cast<int>((n + 255) / 256);
-    g.total_units = g.tiles_m * g.tiles_n * g.nchunks;
+    g.tiles_m = tiles_m;
+    g.tiles_n = tiles_n;
+    if (fused) {
+      g.total_units = static_cast<int>(tiles);
+      g.fused_words = words;
+      const int grid = static_cast<int>(std::min<int64_t>(tiles, ctx->num_sms));
+      g.scratch = static_cast<uint64_t*>(
+          ctx->scratch.get(sizeof(uint64_t) * static_cast<size_t>(grid) * words * 256 * kBlockM));
+      g.qa = qa;
+      g.qb = qb;
+      g.w_last = w_last;
+      g.c = dc;
+      g.ldc = ldc;
+      g.axpby = axpby ? 1 : 0;
+      g.alpha = alpha;
+      g.beta = beta;
+      g.cin = dcin;
+      g.ldcin = ldcin;
+      OZ_CUDA(launch_gemm_i8(&tma, &tmb, g, ctx->num_sms, st, &launches));
+      if (ctx->timing) {
+        OZ_CUDA(cudaEventRecord(ev[2], st));
+        OZ_CUDA(cudaEventRecord(ev[3], st));
+        ctx->pending_events.push_back(ev);
+      }
+      ctx->launches += launches;
+      return nullptr;
+    }
+    const int64_t ldp = round_up(n, 4);
+    const int64_t plane = m * ldp;
+    int32_t* planes = static_cast<int32_t*>(
+        ctx->planes.get(sizeof(int32_t) * static_cast<size_t>(plane) * cp.chunks.size()));
+    g.total_units = static_cast<int>(tiles * g.nchunks);
     g.planes = planes;
     g.plane_stride = plane;
     g.ldp = ldp;
@@ -778,7 +830,7 @@ int ozgpu_dgemm_device(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const do
     if (v.capacity_error || v.precision_error) throw std::domain_error(v.message);
     std::lock_guard<std::mutex> lock(ctx->mu);
     OZ_CUDA(cudaSetDevice(ctx->device));
-    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
     run_multiply(ctx, m, n, k, a, lda, b, ldb, c, ldc, cfg, *plan, st, dev_status, false, 1.0,
                  0.0, nullptr, 0);
     if (diag) *diag = make_diag(*plan, cfg, m, n, k, 0);

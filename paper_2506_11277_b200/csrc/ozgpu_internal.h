@@ -36,6 +36,18 @@ struct GemmArgs {
   int32_t* planes;    // [nchunks][m][ldp] int32 chunk sums
   int64_t plane_stride;
   int64_t ldp;
+  // fused exact epilogue (fused_words = W > 0; units are tiles)
+  int fused_words;
+  uint64_t* scratch;  // per CTA: W x 256 x 128 words
+  const int* qa;
+  const int* qb;
+  long w_last;
+  double* c;
+  int64_t ldc;
+  int axpby;
+  double alpha, beta;
+  const double* cin;
+  int64_t ldcin;
 };
 
 struct CombineArgs {

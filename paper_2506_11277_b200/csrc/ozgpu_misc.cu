@@ -1,0 +1,301 @@
+// Combine, kappa-profile and integer_gemm helper kernels of the B200-native
+// Ozaki-I FP64 GEMM (scheme.cpp:267-355, analysis.cpp:25-68, mma_sim.cpp:76-125).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ozgpu_internal.h"
+#include "ozgpu_numeric.h"
+
+namespace ozgpu {
+
+__device__ __forceinline__ unsigned long long abs_bits_m(double x) {
+  return static_cast<unsigned long long>(__double_as_longlong(x)) & 0x7FFFFFFFFFFFFFFFULL;
+}
+
+// ----------------------------------------------------------------------------
+// Exact combine: V = sum_chunks S_c << shift_c as a W-word two's-complement
+// integer, C = RN(V * 2^(qa_i + qb_j + w_last)) exactly as ExactValue::to_double.
+// ----------------------------------------------------------------------------
+
+template <int W>
+__global__ void __launch_bounds__(256) combine_exact_kernel(const CombineArgs p) {
+  const int64_t total = static_cast<int64_t>(p.m) * p.n;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = idx / p.n, j = idx - i * p.n;
+    uint64_t v[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) v[w] = 0;
+    const int32_t* src = p.planes + i * p.ldp + j;
+    for (int c = 0; c < p.nchunks; ++c) {
+      const int32_t s = __ldg(src + c * p.plane_stride);
+      if (s != 0) words_add_shifted<W>(v, s, p.chunks[c].shift);
+    }
+    const long e = static_cast<long>(__ldg(p.qa + i)) + __ldg(p.qb + j) + p.w_last;
+    double r = round_words<W>(v, e);
+    if (p.axpby)  // two roundings, no FMA contraction (scheme.cpp:369-370)
+      r = __dadd_rn(__dmul_rn(p.alpha, r), __dmul_rn(p.beta, p.cin[i * p.ldcin + j]));
+    p.c[i * p.ldc + j] = r;
+  }
+}
+
+// Sequential FP64 accumulation in the reference order (d ascending, l
+// ascending) with the TwoSum inexact counter (scheme.cpp:173-215).
+__global__ void __launch_bounds__(256) combine_sequential_kernel(const CombineArgs p) {
+  const int64_t total = static_cast<int64_t>(p.m) * p.n;
+  int local_max = 0;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = idx / p.n, j = idx - i * p.n;
+    const int32_t* src = p.planes + i * p.ldp + j;
+    const long qe = static_cast<long>(__ldg(p.qa + i)) + __ldg(p.qb + j);
+    double acc = 0.0;
+    int inexact = 0;
+    long long pending = 0;  // integer chain of one reference chunk
+    for (int c = 0; c < p.nchunks; ++c) {
+      pending += __ldg(src + c * p.plane_stride);
+      const ChunkDesc cd = p.chunks[c];
+      if (!cd.flush) continue;
+      const long long s = pending;
+      pending = 0;
+      const long wexp = -static_cast<long>(cd.d + 2) * p.width + (p.mode == 1 ? 2 : 0);
+      double term = s != 0 ? ldexp_rn(__ll2double_rn(s), qe + wexp) : 0.0;
+      double sum = __dadd_rn(acc, term);
+      double bp = __dsub_rn(sum, acc);
+      double err = __dadd_rn(__dsub_rn(acc, __dsub_rn(sum, bp)), __dsub_rn(term, bp));
+      inexact += err != 0.0;
+      acc = sum;
+    }
+    local_max = inexact > local_max ? inexact : local_max;
+    double r = acc;
+    if (p.axpby)  // two roundings, no FMA contraction (scheme.cpp:369-370)
+      r = __dadd_rn(__dmul_rn(p.alpha, r), __dmul_rn(p.beta, p.cin[i * p.ldcin + j]));
+    p.c[i * p.ldc + j] = r;
+  }
+  if (local_max) atomicMax(p.realized_psi, local_max);
+}
+
+// ----------------------------------------------------------------------------
+// kappa profile (analysis.cpp:25-47): per-row / per-column max and min
+// nonzero magnitude.
+// ----------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(256) row_profile_kernel(const double* __restrict__ a,
+                                                          int64_t lda, int64_t m, int64_t k,
+                                                          double* __restrict__ ratios,
+                                                          int* __restrict__ zero_flag) {
+  __shared__ unsigned long long rmax[8], rmin[8];
+  for (int64_t row = blockIdx.x; row < m; row += gridDim.x) {
+    unsigned long long mx = 0, mn = ~0ULL;
+    for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
+      unsigned long long b = abs_bits_m(__ldg(a + row * lda + j));
+      if (b) {
+        mx = b > mx ? b : mx;
+        mn = b < mn ? b : mn;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      unsigned long long t = __shfl_xor_sync(0xFFFFFFFFu, mx, o);
+      unsigned long long u = __shfl_xor_sync(0xFFFFFFFFu, mn, o);
+      mx = t > mx ? t : mx;
+      mn = u < mn ? u : mn;
+    }
+    if ((threadIdx.x & 31) == 0) {
+      rmax[threadIdx.x >> 5] = mx;
+      rmin[threadIdx.x >> 5] = mn;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
+        mx = rmax[w] > mx ? rmax[w] : mx;
+        mn = rmin[w] < mn ? rmin[w] : mn;
+      }
+      if (mx == 0) {
+        ratios[row] = 1.0;
+        *zero_flag = 1;
+      } else {
+        ratios[row] = __ddiv_rn(__longlong_as_double(static_cast<long long>(mx)),
+                                __longlong_as_double(static_cast<long long>(mn)));
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) col_profile_kernel(const double* __restrict__ b,
+                                                          int64_t ldb, int64_t k, int64_t n,
+                                                          int64_t rows_per,
+                                                          unsigned long long* __restrict__ colmax,
+                                                          unsigned long long* __restrict__ colmin) {
+  int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per;
+  int64_t r1 = r0 + rows_per < k ? r0 + rows_per : k;
+  unsigned long long mx = 0, mn = ~0ULL;
+  for (int64_t r = r0; r < r1; ++r) {
+    unsigned long long t = abs_bits_m(__ldg(b + r * ldb + j));
+    if (t) {
+      mx = t > mx ? t : mx;
+      mn = t < mn ? t : mn;
+    }
+  }
+  if (mx) atomicMax(colmax + j, mx);
+  if (mn != ~0ULL) atomicMin(colmin + j, mn);
+}
+
+// ----------------------------------------------------------------------------
+// integer_gemm debug hook helpers (mma_sim.cpp:76-125)
+// ----------------------------------------------------------------------------
+
+// int64 (rows x cols) -> int8 K-major rows of length kp: transpose=0 keeps
+// rows (X, m x k -> [m][kp]); transpose=1 emits columns (Y, k x n -> [n][kp]).
+__global__ void pack_i8_kernel(const int64_t* __restrict__ x, int64_t rows, int64_t cols,
+                               int transpose, int64_t kp, int8_t* __restrict__ out) {
+  const int64_t outer = transpose ? cols : rows;
+  const int64_t total = outer * kp;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t o = idx / kp, kk = idx - o * kp;
+    int64_t inner = transpose ? rows : cols;
+    int8_t v = 0;
+    if (kk < inner) v = static_cast<int8_t>(transpose ? x[kk * cols + o] : x[o * cols + kk]);
+    out[idx] = v;
+  }
+}
+
+// Exact CUDA-core integer GEMM with the reference's per-MAC range check
+// (mma_sim.cpp:103-112); records the first overflowing (row-major) element.
+__global__ void integer_gemm_exact_kernel(const int64_t* __restrict__ x,
+                                          const int64_t* __restrict__ y,
+                                          const int64_t* __restrict__ c, int64_t* __restrict__ out,
+                                          int64_t m, int64_t k, int64_t n, int acc_width,
+                                          unsigned long long* first_overflow) {
+  const int64_t total = m * n;
+  const __int128 lo = -(static_cast<__int128>(1) << acc_width);
+  const __int128 hi = (static_cast<__int128>(1) << acc_width) - 1;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t i = idx / n, j = idx - i * n;
+    __int128 acc = c ? c[idx] : 0;
+    bool ovf = false;
+    for (int64_t r = 0; r < k; ++r) {
+      acc += static_cast<__int128>(x[i * k + r]) * y[r * n + j];
+      if (acc < lo || acc > hi) {
+        ovf = true;
+        break;
+      }
+    }
+    if (ovf)
+      atomicMin(first_overflow, static_cast<unsigned long long>(idx));
+    else
+      out[idx] = static_cast<int64_t>(acc);
+  }
+}
+
+__global__ void plane_to_i64_kernel(const int32_t* __restrict__ plane, int64_t ldp,
+                                    const int64_t* __restrict__ c, int64_t* __restrict__ out,
+                                    int64_t m, int64_t n) {
+  const int64_t total = m * n;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t i = idx / n, j = idx - i * n;
+    out[idx] = static_cast<int64_t>(plane[i * ldp + j]) + (c ? c[idx] : 0);
+  }
+}
+
+static inline int grid_for(int64_t work, int per_block, int cap = 148 * 16) {
+  int64_t g = (work + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  return static_cast<int>(g < cap ? g : cap);
+}
+
+
+cudaError_t launch_combine_exact(const CombineArgs& args, int words, cudaStream_t st,
+                                 int64_t* launches) {
+  int64_t total = static_cast<int64_t>(args.m) * args.n;
+  if (total == 0) return cudaSuccess;
+  int grid = grid_for(total, 256);
+  switch (words) {
+    case 2: combine_exact_kernel<2><<<grid, 256, 0, st>>>(args); break;
+    case 3: combine_exact_kernel<3><<<grid, 256, 0, st>>>(args); break;
+    case 4: combine_exact_kernel<4><<<grid, 256, 0, st>>>(args); break;
+    case 6: combine_exact_kernel<6><<<grid, 256, 0, st>>>(args); break;
+    case 8: combine_exact_kernel<8><<<grid, 256, 0, st>>>(args); break;
+    case 12: combine_exact_kernel<12><<<grid, 256, 0, st>>>(args); break;
+    case 16: combine_exact_kernel<16><<<grid, 256, 0, st>>>(args); break;
+    default: return cudaErrorInvalidValue;
+  }
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine_sequential(const CombineArgs& args, cudaStream_t st,
+                                      int64_t* launches) {
+  int64_t total = static_cast<int64_t>(args.m) * args.n;
+  if (total == 0) return cudaSuccess;
+  combine_sequential_kernel<<<grid_for(total, 256), 256, 0, st>>>(args);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_row_profile(const double* a, int64_t lda, int64_t m, int64_t k,
+                               double* ratios, int* zero_flag, cudaStream_t st,
+                               int64_t* launches) {
+  if (m == 0) return cudaSuccess;
+  int grid = static_cast<int>(m < 148 * 32 ? m : 148 * 32);
+  row_profile_kernel<<<grid, 256, 0, st>>>(a, lda, m, k, ratios, zero_flag);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_col_profile(const double* b, int64_t ldb, int64_t k, int64_t n,
+                               unsigned long long* colmax, unsigned long long* colmin,
+                               cudaStream_t st, int64_t* launches) {
+  if (n == 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * n, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(colmin, 0xFF, sizeof(unsigned long long) * n, st);
+  if (e != cudaSuccess) return e;
+  int64_t col_blocks = (n + 255) / 256;
+  int64_t splits = (148 * 8 + col_blocks - 1) / col_blocks;
+  if (splits > k) splits = k > 0 ? k : 1;
+  if (splits > 65535) splits = 65535;
+  int64_t rows_per = k > 0 ? (k + splits - 1) / splits : 0;
+  dim3 grid(static_cast<unsigned>(col_blocks), static_cast<unsigned>(splits));
+  col_profile_kernel<<<grid, 256, 0, st>>>(b, ldb, k, n, rows_per, colmax, colmin);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_i8(const int64_t* x, int64_t rows, int64_t cols, int transpose,
+                           int64_t kp, int8_t* out, cudaStream_t st, int64_t* launches) {
+  int64_t total = (transpose ? cols : rows) * kp;
+  if (total == 0) return cudaSuccess;
+  pack_i8_kernel<<<grid_for(total, 256), 256, 0, st>>>(x, rows, cols, transpose, kp, out);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_integer_gemm_exact(const int64_t* x, const int64_t* y, const int64_t* c,
+                                      int64_t* out, int64_t m, int64_t k, int64_t n,
+                                      int acc_width, unsigned long long* first_overflow,
+                                      cudaStream_t st, int64_t* launches) {
+  if (m * n == 0) return cudaSuccess;
+  integer_gemm_exact_kernel<<<grid_for(m * n, 128), 128, 0, st>>>(x, y, c, out, m, k, n,
+                                                                  acc_width, first_overflow);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_plane_to_i64(const int32_t* plane, int64_t ldp, const int64_t* c,
+                                int64_t* out, int64_t m, int64_t n, cudaStream_t st,
+                                int64_t* launches) {
+  if (m * n == 0) return cudaSuccess;
+  plane_to_i64_kernel<<<grid_for(m * n, 256), 256, 0, st>>>(plane, ldp, c, out, m, n);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+}  // namespace ozgpu
+

@@ -1,0 +1,444 @@
+// Slicing kernels of the B200-native Ozaki-I FP64 GEMM (HBM-bound):
+// per-row / per-column block scales and the FP64 -> int8 slice split
+// (proj/src/slicing.cpp:67-132, fpcore.cpp:58-87).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ozgpu_internal.h"
+#include "ozgpu_numeric.h"
+
+namespace ozgpu {
+// ----------------------------------------------------------------------------
+// Slicing (proj/src/slicing.cpp:67-132; fpcore.cpp:58-87)
+// ----------------------------------------------------------------------------
+
+// Absolute value bits of a double; positive doubles order like their bits.
+__device__ __forceinline__ unsigned long long abs_bits(double x) {
+  return static_cast<unsigned long long>(__double_as_longlong(x)) & 0x7FFFFFFFFFFFFFFFULL;
+}
+
+// Input status bits: 1 = Inf/NaN (split rejects these, slicing.cpp:88),
+// 2 = negative zero (multiply also rejects these, matrix.cpp:22-29).
+__device__ __forceinline__ int dirty(double x) {
+  unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+  return (((b >> 52) & 0x7FF) == 0x7FF ? 1 : 0) | (b == 0x8000000000000000ULL ? 2 : 0);
+}
+
+// Block-scale exponent from the max |x| bits: ilogb(max) + 1, 0 for a zero
+// block (slicing.cpp:92, fpcore.cpp:83-87).  Handles subnormal maxima.
+__device__ __forceinline__ int scale_from_maxbits(unsigned long long mb) {
+  if (mb == 0) return 0;
+  int be = static_cast<int>(mb >> 52);
+  if (be > 0) return be - 1023 + 1;
+  int top = 63 - __clzll(static_cast<long long>(mb));  // frac's leading bit
+  return top - 1074 + 1;
+}
+
+// Writes the `count` slices of 8 consecutive entries (values v[0..8)) of
+// one row / column with block exponent q.  Out layout: out[l * plane + off + e].
+template <typename OutT>
+__device__ __forceinline__ void emit_slices8(const double* v, int q, int width, int count,
+                                             int mode, OutT* out, int64_t plane, int64_t off) {
+  SliceEntry ent[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) ent[e] = make_slice_entry(v[e], q, width, count, mode);
+  for (int l = 0; l < count; ++l) {
+    if constexpr (sizeof(OutT) == 1) {
+      unsigned long long packed = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        long long s = slice_of(ent[e], l, width, count, mode);
+        packed |= (static_cast<unsigned long long>(s) & 0xFFULL) << (8 * e);
+      }
+      *reinterpret_cast<unsigned long long*>(out + l * plane + off) = packed;
+    } else {
+      long long s[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s[e] = slice_of(ent[e], l, width, count, mode);
+      longlong2* dst = reinterpret_cast<longlong2*>(out + l * plane + off);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) dst[e] = make_longlong2(s[2 * e], s[2 * e + 1]);
+    }
+  }
+}
+
+// One CTA per row (grid-stride).  Pass 1: max |a| + cleanliness over the
+// row; pass 2: s slices of 8 consecutive entries per thread, written as
+// K-major rows of length kp (zero padded past k).
+template <typename OutT>
+__global__ void __launch_bounds__(256) slice_rows_kernel(const double* __restrict__ a,
+                                                         int64_t lda, int64_t m, int64_t k,
+                                                         int64_t kp, int width, int count,
+                                                         int mode, OutT* __restrict__ out,
+                                                         int* __restrict__ scales,
+                                                         int* __restrict__ status) {
+  __shared__ unsigned long long red[8];
+  const int64_t plane = m * kp;
+  for (int64_t row = blockIdx.x; row < m; row += gridDim.x) {
+    const double* ar = a + row * lda;
+    unsigned long long mx = 0;
+    int bad = 0;
+    for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
+      double x = __ldg(ar + j);
+      bad |= dirty(x);
+      unsigned long long b = abs_bits(x);
+      mx = b > mx ? b : mx;
+    }
+    if (bad) atomicOr(status, bad);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      unsigned long long t = __shfl_xor_sync(0xFFFFFFFFu, mx, o);
+      mx = t > mx ? t : mx;
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      unsigned long long t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        unsigned long long u = __shfl_xor_sync(0xFFFFFFFFu, t, o);
+        t = u > t ? u : t;
+      }
+      if (threadIdx.x == 0) red[0] = t;
+    }
+    __syncthreads();
+    const int q = scale_from_maxbits(red[0]);
+    if (threadIdx.x == 0) scales[row] = q;
+    for (int64_t g = threadIdx.x; g < kp / 8; g += blockDim.x) {
+      double v[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        int64_t j = g * 8 + e;
+        v[e] = j < k ? __ldg(ar + j) : 0.0;
+      }
+      emit_slices8<OutT>(v, q, width, count, mode, out, plane, row * kp + g * 8);
+    }
+    __syncthreads();
+  }
+}
+
+// Column max |b| + cleanliness: thread per column, rows split over gridDim.y.
+__global__ void __launch_bounds__(256) colmax_kernel(const double* __restrict__ b, int64_t ldb,
+                                                     int64_t k, int64_t n, int64_t rows_per,
+                                                     unsigned long long* __restrict__ colmax,
+                                                     int* __restrict__ status) {
+  int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per;
+  int64_t r1 = r0 + rows_per < k ? r0 + rows_per : k;
+  unsigned long long mx = 0;
+  int bad = 0;
+  for (int64_t r = r0; r < r1; ++r) {
+    double x = __ldg(b + r * ldb + j);
+    bad |= dirty(x);
+    unsigned long long t = abs_bits(x);
+    mx = t > mx ? t : mx;
+  }
+  if (bad) atomicOr(status, bad);
+  if (mx) atomicMax(colmax + j, mx);
+}
+
+// 64 (k) x 64 (n) tile transpose-and-slice: B is k x n row-major; slices are
+// written K-major as out[l][n][kp] (the tcgen05 B operand layout).
+template <typename OutT>
+__global__ void __launch_bounds__(256) slice_cols_kernel(
+    const double* __restrict__ b, int64_t ldb, int64_t k, int64_t n, int64_t kp, int width,
+    int count, int mode, const unsigned long long* __restrict__ colmax, OutT* __restrict__ out,
+    int* __restrict__ scales) {
+  __shared__ double tile[64][65];
+  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * 64;
+  const int64_t n0 = static_cast<int64_t>(blockIdx.y) * 64;
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+  for (int rr = ty; rr < 64; rr += 4) {
+    int64_t r = k0 + rr, c = n0 + tx;
+    tile[tx][rr] = (r < k && c < n) ? __ldg(b + r * ldb + c) : 0.0;
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x < 64 && n0 + threadIdx.x < n)
+    scales[n0 + threadIdx.x] = scale_from_maxbits(colmax[n0 + threadIdx.x]);
+  const int64_t plane = n * kp;
+  for (int item = threadIdx.x; item < 64 * 8; item += blockDim.x) {
+    int nl = item >> 3, g = item & 7;
+    int64_t col = n0 + nl;
+    if (col >= n) continue;
+    int64_t kk = k0 + g * 8;
+    if (kk >= kp) continue;
+    int q = scale_from_maxbits(colmax[col]);
+    double v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = tile[nl][g * 8 + e];
+    emit_slices8<OutT>(v, q, width, count, mode, out, plane, col * kp + kk);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Fast path (the product's default: truncate mode, t <= 7, int8 slices).
+// The fraction bits of |x| / 2^q are cut into 63-bit windows holding
+// 63 / T whole slices each, so every slice is one constant shift + mask of a
+// window instead of a per-slice variable-shift field extraction; signs are
+// applied to 4 packed bytes at a time.  Bit-identical to slice_of() in
+// truncate mode (extract_field, slicing.cpp:35-45).
+// ----------------------------------------------------------------------------
+
+template <int T>
+__device__ __forceinline__ void emit8_trunc_i8(const double (&v)[8], int q, int count,
+                                               int8_t* __restrict__ out, int64_t plane,
+                                               int64_t off) {
+  constexpr int SPW = 63 / T;  // slices per window
+  constexpr int WB = SPW * T;  // window bits
+  constexpr uint64_t WMASK = (WB == 64) ? ~0ULL : ((1ULL << WB) - 1);
+  constexpr uint32_t TMASK = (1u << T) - 1;
+  uint64_t sig[8];
+  int lsb[8];
+  uint32_t neg_lo = 0, neg_hi = 0;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    uint64_t bits = dbl_bits(v[e]);
+    if (bits >> 63) {
+      if (e < 4)
+        neg_lo |= 0xFFu << (8 * e);
+      else
+        neg_hi |= 0xFFu << (8 * (e - 4));
+    }
+    bits &= 0x7FFFFFFFFFFFFFFFULL;
+    const uint64_t biased = bits >> 52;
+    const uint64_t frac = bits & 0xFFFFFFFFFFFFFULL;
+    sig[e] = biased ? (frac | 0x10000000000000ULL) : frac;
+    const int ex = biased ? static_cast<int>(biased) - 1023 : -1022;
+    lsb[e] = q + 52 - ex;
+  }
+  for (int j = 0; j * SPW < count; ++j) {
+    uint64_t w[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int sh = WB * (j + 1) - lsb[e];
+      uint64_t x = sh >= 0 ? (sh < 64 ? (sig[e] << sh) : 0ULL) : (sh > -64 ? (sig[e] >> -sh) : 0ULL);
+      w[e] = x & WMASK;
+    }
+#pragma unroll
+    for (int i = 0; i < SPW; ++i) {
+      const int l = j * SPW + i;
+      if (l >= count) break;
+      const int s = WB - T * (i + 1);
+      uint32_t lo = 0, hi = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        lo |= (static_cast<uint32_t>(w[e] >> s) & TMASK) << (8 * e);
+        hi |= (static_cast<uint32_t>(w[e + 4] >> s) & TMASK) << (8 * e);
+      }
+      lo = __vsub4(lo ^ neg_lo, neg_lo);
+      hi = __vsub4(hi ^ neg_hi, neg_hi);
+      *reinterpret_cast<uint2*>(out + l * plane + off) = make_uint2(lo, hi);
+    }
+  }
+}
+
+// One warp per row (grid-stride over rows): warp-shuffle max, then slices of
+// 8 consecutive entries per lane (the second read of the row hits L2).
+template <int T, bool VEC>
+__global__ void __launch_bounds__(256) slice_rows_fast_kernel(
+    const double* __restrict__ a, int64_t lda, int64_t m, int64_t k, int64_t kp, int count,
+    int8_t* __restrict__ out, int* __restrict__ scales, int* __restrict__ status) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const int64_t plane = m * kp;
+  for (int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       row < m; row += warps) {
+    const double* ar = a + row * lda;
+    unsigned long long mx = 0;
+    int bad = 0;
+    int64_t j = lane;
+    for (; j + 224 < k; j += 256) {
+      double x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = __ldg(ar + j + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        bad |= dirty(x[u]);
+        unsigned long long b = abs_bits(x[u]);
+        mx = b > mx ? b : mx;
+      }
+    }
+    for (; j < k; j += 32) {
+      double x = __ldg(ar + j);
+      bad |= dirty(x);
+      unsigned long long b = abs_bits(x);
+      mx = b > mx ? b : mx;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      unsigned long long t = __shfl_xor_sync(0xFFFFFFFFu, mx, o);
+      mx = t > mx ? t : mx;
+    }
+    bad = __reduce_or_sync(0xFFFFFFFFu, bad);
+    if (lane == 0) {
+      if (bad) atomicOr(status, bad);
+      scales[row] = scale_from_maxbits(mx);
+    }
+    const int q = scale_from_maxbits(mx);
+    for (int64_t g = lane; g < kp / 8; g += 32) {
+      double v[8];
+      const int64_t j0 = g * 8;
+      if (VEC && j0 + 8 <= k) {
+        const double2* p2 = reinterpret_cast<const double2*>(ar + j0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          double2 t2 = __ldg(p2 + u);
+          v[2 * u] = t2.x;
+          v[2 * u + 1] = t2.y;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = j0 + e < k ? __ldg(ar + j0 + e) : 0.0;
+      }
+      emit8_trunc_i8<T>(v, q, count, out, plane, row * kp + j0);
+    }
+  }
+}
+
+// 128 (k) x 32 (n) tile transpose-and-slice into K-major [l][n][kp] int8.
+// Smem holds the tile column-major in 16-byte units with an XOR swizzle so
+// both the row-wise fill and the 8-entry column reads are conflict-light.
+template <int T>
+__global__ void __launch_bounds__(256) slice_cols_fast_kernel(
+    const double* __restrict__ b, int64_t ldb, int64_t k, int64_t n, int64_t kp, int count,
+    const unsigned long long* __restrict__ colmax, int8_t* __restrict__ out,
+    int* __restrict__ scales) {
+  constexpr int TK = 128, TN = 32, STRIDE = TK + 2;  // doubles per column (padded)
+  __shared__ __align__(16) double tile[TN * STRIDE];
+  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * TK;
+  const int64_t n0 = static_cast<int64_t>(blockIdx.y) * TN;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // swizzled position of row r in column c: 16-byte unit (r >> 1) ^ ((r >> 3) & 7)
+  auto pos = [](int c, int r) {
+    int u = r >> 1;
+    return c * STRIDE + ((u ^ ((u >> 2) & 7)) << 1) + (r & 1);
+  };
+  for (int r = warp; r < TK; r += 8) {
+    const int64_t kr = k0 + r, c = n0 + lane;
+    tile[pos(lane, r)] = (kr < k && c < n) ? __ldg(b + kr * ldb + c) : 0.0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < TN && n0 + threadIdx.x < n)
+    scales[n0 + threadIdx.x] = scale_from_maxbits(colmax[n0 + threadIdx.x]);
+  __syncthreads();
+  const int64_t plane = n * kp;
+  // item = (column, group of 8 rows); groups fastest so a warp writes 2
+  // columns x 128 contiguous bytes per slice
+  for (int item = threadIdx.x; item < TN * (TK / 8); item += blockDim.x) {
+    const int c = item / (TK / 8), g = item % (TK / 8);
+    const int64_t col = n0 + c, kk = k0 + g * 8;
+    if (col >= n || kk >= kp) continue;
+    const int q = scale_from_maxbits(colmax[col]);
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double2 t2 = *reinterpret_cast<const double2*>(&tile[pos(c, g * 8 + 2 * u)]);
+      v[2 * u] = t2.x;
+      v[2 * u + 1] = t2.y;
+    }
+    emit8_trunc_i8<T>(v, q, count, out, plane, col * kp + kk);
+  }
+}
+
+static inline int grid_for(int64_t work, int per_block, int cap = 148 * 16) {
+  int64_t g = (work + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  return static_cast<int>(g < cap ? g : cap);
+}
+
+template <int T>
+static void launch_rows_fast_t(const double* a, int64_t lda, int64_t m, int64_t k, int64_t kp,
+                               int count, int8_t* out, int* scales, int* status, cudaStream_t st) {
+  const bool vec = (reinterpret_cast<uintptr_t>(a) & 15) == 0 && (lda & 1) == 0;
+  const int grid = grid_for(m, 8, 148 * 8);
+  if (vec)
+    slice_rows_fast_kernel<T, true><<<grid, 256, 0, st>>>(a, lda, m, k, kp, count, out, scales,
+                                                          status);
+  else
+    slice_rows_fast_kernel<T, false><<<grid, 256, 0, st>>>(a, lda, m, k, kp, count, out, scales,
+                                                           status);
+}
+
+template <int T>
+static void launch_cols_fast_t(const double* b, int64_t ldb, int64_t k, int64_t n, int64_t kp,
+                               int count, const unsigned long long* colmax, int8_t* out,
+                               int* scales, cudaStream_t st) {
+  dim3 grid(static_cast<unsigned>((kp + 127) / 128), static_cast<unsigned>((n + 31) / 32));
+  slice_cols_fast_kernel<T><<<grid, 256, 0, st>>>(b, ldb, k, n, kp, count, colmax, out, scales);
+}
+
+cudaError_t launch_slice_rows(const double* a, int64_t lda, int64_t m, int64_t k, int64_t kp,
+                              int width, int count, int mode, void* out, int out_is_i64,
+                              int* scales, int* status, cudaStream_t st, int64_t* launches) {
+  if (m == 0) return cudaSuccess;
+  if (!out_is_i64 && mode == 0 && width >= 1 && width <= 7) {
+    int8_t* o = static_cast<int8_t*>(out);
+    switch (width) {
+      case 7: launch_rows_fast_t<7>(a, lda, m, k, kp, count, o, scales, status, st); break;
+      case 6: launch_rows_fast_t<6>(a, lda, m, k, kp, count, o, scales, status, st); break;
+      case 5: launch_rows_fast_t<5>(a, lda, m, k, kp, count, o, scales, status, st); break;
+      case 4: launch_rows_fast_t<4>(a, lda, m, k, kp, count, o, scales, status, st); break;
+      case 3: launch_rows_fast_t<3>(a, lda, m, k, kp, count, o, scales, status, st); break;
+      case 2: launch_rows_fast_t<2>(a, lda, m, k, kp, count, o, scales, status, st); break;
+      default: launch_rows_fast_t<1>(a, lda, m, k, kp, count, o, scales, status, st); break;
+    }
+    ++*launches;
+    return cudaGetLastError();
+  }
+  int grid = static_cast<int>(m < 148 * 32 ? m : 148 * 32);
+  if (out_is_i64)
+    slice_rows_kernel<long long><<<grid, 256, 0, st>>>(a, lda, m, k, kp, width, count, mode,
+                                                       static_cast<long long*>(out), scales,
+                                                       status);
+  else
+    slice_rows_kernel<int8_t><<<grid, 256, 0, st>>>(a, lda, m, k, kp, width, count, mode,
+                                                    static_cast<int8_t*>(out), scales, status);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_slice_cols(const double* b, int64_t ldb, int64_t k, int64_t n, int64_t kp,
+                              int width, int count, int mode, void* out, int out_is_i64,
+                              int* scales, unsigned long long* colmax, int* status,
+                              cudaStream_t st, int64_t* launches) {
+  if (n == 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * n, st);
+  if (e != cudaSuccess) return e;
+  {
+    int64_t col_blocks = (n + 255) / 256;
+    int64_t splits = (148 * 8 + col_blocks - 1) / col_blocks;
+    if (splits > k) splits = k > 0 ? k : 1;
+    if (splits > 65535) splits = 65535;
+    int64_t rows_per = k > 0 ? (k + splits - 1) / splits : 0;
+    dim3 grid(static_cast<unsigned>(col_blocks), static_cast<unsigned>(splits));
+    colmax_kernel<<<grid, 256, 0, st>>>(b, ldb, k, n, rows_per, colmax, status);
+    ++*launches;
+  }
+  if (!out_is_i64 && mode == 0 && width >= 1 && width <= 7 && kp % 128 == 0) {
+    int8_t* o = static_cast<int8_t*>(out);
+    switch (width) {
+      case 7: launch_cols_fast_t<7>(b, ldb, k, n, kp, count, colmax, o, scales, st); break;
+      case 6: launch_cols_fast_t<6>(b, ldb, k, n, kp, count, colmax, o, scales, st); break;
+      case 5: launch_cols_fast_t<5>(b, ldb, k, n, kp, count, colmax, o, scales, st); break;
+      case 4: launch_cols_fast_t<4>(b, ldb, k, n, kp, count, colmax, o, scales, st); break;
+      case 3: launch_cols_fast_t<3>(b, ldb, k, n, kp, count, colmax, o, scales, st); break;
+      case 2: launch_cols_fast_t<2>(b, ldb, k, n, kp, count, colmax, o, scales, st); break;
+      default: launch_cols_fast_t<1>(b, ldb, k, n, kp, count, colmax, o, scales, st); break;
+    }
+    ++*launches;
+    return cudaGetLastError();
+  }
+  dim3 grid2(static_cast<unsigned>((kp + 63) / 64), static_cast<unsigned>((n + 63) / 64));
+  if (out_is_i64)
+    slice_cols_kernel<long long><<<grid2, 256, 0, st>>>(b, ldb, k, n, kp, width, count, mode,
+                                                        colmax, static_cast<long long*>(out),
+                                                        scales);
+  else
+    slice_cols_kernel<int8_t><<<grid2, 256, 0, st>>>(b, ldb, k, n, kp, width, count, mode,
+                                                     colmax, static_cast<int8_t*>(out), scales);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+}  // namespace ozgpu

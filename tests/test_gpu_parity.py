@@ -230,3 +230,29 @@ def test_native_kernels_launched(oz):
     before = oz.kernel_launches()
     oz.multiply(np.ones((8, 8)), np.ones((8, 8)), cfg, oz.make_plan(cfg, 8, 2, 2))
     assert oz.kernel_launches() - before >= 4
+
+
+@pytest.mark.parametrize("mode", ["fused", "split"])
+def test_epilogue_modes_match_reference(oz, ref, mode, monkeypatch):
+    """Both GEMM epilogues (fused exact-integer RMW / split planes + combine)
+    are bit-exact, incl. ragged tiles and 3-word exact values."""
+    monkeypatch.setenv("OZGPU_EPILOGUE", mode)
+    rng = np.random.default_rng(77)
+    cfg = oz.MmaConfig.int8_int32()
+    for (m, k, n) in [(128, 256, 256), (300, 500, 700), (1000, 128, 513)]:
+        a = uniform(m, k, rng)
+        b = random_matrix(k, n, rng, -30, 30, 0.02)
+        for (sa, sb), sched in [((4, 4), 1), ((8, 8), 1), ((13, 12), 1), ((16, 17), 1),
+                                ((6, 7), 0)]:
+            plan = oz.make_plan(cfg, k, sa, sb, oz.ScheduleKind(sched))
+            got = oz.multiply(a, b, cfg, plan).c
+            want, _ = ref.ref_multiply(a, b, sa, sb, sched)
+            assert bits_equal(got, want), (m, k, n, sa, sb, mismatch_report(got, want))
+    # axpby through the fused epilogue
+    a = uniform(256, 384, rng)
+    b = uniform(384, 512, rng)
+    c = uniform(256, 512, rng)
+    plan = oz.make_plan(cfg, 384, 7, 7)
+    got = oz.multiply_axpby(1.5, a, b, -0.25, c, cfg, plan).c
+    want = ref.ref_multiply_axpby(1.5, a, b, -0.25, c, 7, 7)
+    assert bits_equal(got, want)
