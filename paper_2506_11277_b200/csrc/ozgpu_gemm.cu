@@ -286,6 +286,187 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 }
 
+// ----------------------------------------------------------------------------
+// CTA-pair variant (split mode): a cluster of 2 CTAs on one TPC computes a
+// 256 x 256 tile with tcgen05.mma.cta_group::2 (M=256, N=256, K=32) issued by
+// the leader CTA.  Each CTA stages its own 128 A rows and 128 of the 256 B
+// rows per k-block (32 KB / stage, 6 stages), so per-SM operand traffic from
+// L2 drops from 48 KB to 32 KB per 128x256x128 of work versus the 1-CTA tile.
+// The peers' TMA transactions land on the leader's full barrier; the
+// leader's commits multicast to both CTAs' empty / tmem-full barriers; the
+// epilogue warps of both CTAs release the accumulator on the leader.
+// ----------------------------------------------------------------------------
+
+constexpr int kPairStages = 6;
+constexpr int kPairHalfBytes = 128 * kBlockK;             // 16 KB (A or B half)
+constexpr int kPairStageBytes = 2 * kPairHalfBytes;       // per CTA
+constexpr int kSmemPair = kPairStages * kPairStageBytes + 1024 + 256;
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+    gemm_i8_pair_kernel(const __grid_constant__ CUtensorMap tma,
+                        const __grid_constant__ CUtensorMap tmb, const GemmArgs p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kPairStages * kPairHalfBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kPairStages * kPairStageBytes);
+  uint64_t* empty = full + kPairStages;
+  uint64_t* tfull = empty + kPairStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1;
+  const int npairs = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kPairStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmb)) : "memory");
+  }
+  if (warp == 2) tmem_alloc_pair(tmem_holder, kTmemCols);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const int tiles = p.tiles_m * p.tiles_n;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer (both CTAs) ----------------
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int unit = pair; unit < p.total_units; unit += npairs) {
+      const int c = unit / tiles;
+      const TileCoord tc = decode_tile(unit - c * tiles, p);
+      const ChunkDesc cd = p.chunks[c];
+      const int arow = tc.tm * 256 + static_cast<int>(rank) * 128;
+      const int brow = tc.tn * kBN + static_cast<int>(rank) * 128;
+      for (int pr = 0; pr < cd.npairs; ++pr) {
+        const int l = cd.l0 + pr;
+        const int h = cd.d + 2 - l;
+        for (int kb = 0; kb < p.kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_expect_tx(&full[stage], 2 * kPairStageBytes);
+          const uint32_t bar = map_to_rank(&full[stage], 0);
+          tma_load_3d_pair(sA + stage * kPairHalfBytes, &tma, bar, kb * kBlockK, arow, l - 1);
+          tma_load_3d_pair(sB + stage * kPairHalfBytes, &tmb, bar, kb * kBlockK, brow, h - 1);
+          if (++stage == kPairStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1 && lane == 0 && leader) {
+    // ---------------- MMA issuer (leader CTA, single thread) ----------------
+    constexpr uint32_t idesc = idesc_i8<256, kBN>();
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int unit = pair; unit < p.total_units; unit += npairs, ++it) {
+      const int c = unit / tiles;
+      const ChunkDesc cd = p.chunks[c];
+      const int acc = it & 1;
+      const uint32_t aphase = (it >> 1) & 1;
+      mbar_wait(&tempty[acc], aphase ^ 1);
+      tc_fence_after();
+      const uint32_t tmem_d = tmem_base + acc * kBN;
+      const int total = cd.npairs * p.kblocks;
+      for (int i = 0; i < total; ++i) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint64_t ad = sdesc_sw128(smem_addr(sA + stage * kPairHalfBytes));
+        const uint64_t bd = sdesc_sw128(smem_addr(sB + stage * kPairHalfBytes));
+#pragma unroll
+        for (int kk = 0; kk < kBlockK / 32; ++kk)
+          tc_mma_i8_pair(tmem_d, ad + 2 * kk, bd + 2 * kk, idesc, (i | kk) != 0);
+        tc_commit_pair(&empty[stage]);
+        if (++stage == kPairStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      tc_commit_pair(&tfull[acc]);
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue (both CTAs): TMEM -> int32 chunk plane ----------------
+    const int q = warp & 3;
+    const uint32_t tempty_leader0 = map_to_rank(&tempty[0], 0);
+    const uint32_t tempty_leader1 = map_to_rank(&tempty[1], 0);
+    int it = 0;
+    for (int unit = pair; unit < p.total_units; unit += npairs, ++it) {
+      const int c = unit / tiles;
+      const TileCoord tc = decode_tile(unit - c * tiles, p);
+      const int acc = it & 1;
+      const uint32_t aphase = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], aphase);
+      tc_fence_after();
+      const int row = tc.tm * 256 + static_cast<int>(rank) * 128 + q * 32 + lane;
+      int32_t* dst = p.planes + static_cast<int64_t>(c) * p.plane_stride +
+                     static_cast<int64_t>(row) * p.ldp;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * kBN;
+#pragma unroll 1
+      for (int s0 = 0; s0 < kBN; s0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(taddr + s0, r);
+        const int col0 = tc.tn * kBN + s0;
+        if (row < p.m) {
+          if (col0 + 32 <= p.n && (p.ldp & 3) == 0) {
+            int4* d4 = reinterpret_cast<int4*>(dst + col0);
+#pragma unroll
+            for (int v = 0; v < 8; ++v)
+              __stcs(d4 + v, make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]));
+          } else {
+            for (int v = 0; v < 32; ++v)
+              if (col0 + v < p.n) dst[col0 + v] = static_cast<int32_t>(r[v]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, kTmemCols);
+  }
+}
+
+cudaError_t launch_gemm_i8_pair(const CUtensorMap* tma, const CUtensorMap* tmb,
+                                const GemmArgs& args, int num_sms, cudaStream_t st,
+                                int64_t* launches) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_i8_pair_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemPair);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  int pairs = num_sms / 2;
+  if (args.total_units < pairs) pairs = args.total_units;
+  if (pairs < 1) return cudaSuccess;
+  gemm_i8_pair_kernel<<<2 * pairs, kGemmThreads, kSmemPair, st>>>(*tma, *tmb, args);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) ++*launches;
+  return e;
+}
+
 template <int W>
 static cudaError_t launch_t(const CUtensorMap* tma, const CUtensorMap* tmb, const GemmArgs& args,
                             int grid, int smem, cudaStream_t st) {

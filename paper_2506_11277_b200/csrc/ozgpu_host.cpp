@@ -371,11 +371,13 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
     const int tiles_n = static_cast<int>((n + 255) / 256);
     const int64_t tiles = static_cast<int64_t>(tiles_m) * tiles_n;
     const long w_last = -static_cast<long>(cp.diagonals + 1) * t + (p.mode == 1 ? 2 : 0);
-    // Fused exact epilogue when the tiles alone fill the GPU and the exact
-    // value fits 2-3 words; otherwise (small problems, sequential strategies,
-    // very wide exact values) split units over (tile, chunk) + combine kernel.
+    // Default: split units over (tile, chunk) writing int32 chunk planes, then
+    // the bandwidth-bound exact combine.  The fused exact epilogue (W-word
+    // RMW in a CTA-private scratch) is opt-in (OZGPU_EPILOGUE=fused): measured
+    // on B200 at 8192^3 (12,12) its scratch traffic evicts operand panels from
+    // L2 (105 GB vs 66 GB DRAM per launch) and loses to split + combine.
     int words = p.strategy == 2 ? exact_words(cp.diagonals, t, cp.chunks.size()) : 0;
-    bool fused = p.strategy == 2 && words <= 3 && tiles >= ctx->num_sms;
+    bool fused = false;
     if (const char* env = std::getenv("OZGPU_EPILOGUE")) {
       if (std::string(env) == "split") fused = false;
       if (std::string(env) == "fused" && p.strategy == 2 && words <= 3) fused = true;
@@ -439,11 +441,23 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
     const int64_t plane = m * ldp;
     int32_t* planes = static_cast<int32_t*>(
         ctx->planes.get(sizeof(int32_t) * static_cast<size_t>(plane) * cp.chunks.size()));
-    g.total_units = static_cast<int>(tiles * g.nchunks);
     g.planes = planes;
     g.plane_stride = plane;
     g.ldp = ldp;
-    OZ_CUDA(launch_gemm_i8(&tma, &tmb, g, ctx->num_sms, st, &launches));
+    // CTA-pair (cta_group::2, 256 x 256 tiles) unless the problem is too
+    // short in m or too small to fill the pairs (OZGPU_CTA_PAIR=0/1 forces).
+    const int pair_tiles = static_cast<int>(((m + 255) / 256) * tiles_n);
+    bool pair = m >= 256 && static_cast<int64_t>(pair_tiles) * g.nchunks >= ctx->num_sms / 2;
+    if (const char* env = std::getenv("OZGPU_CTA_PAIR")) pair = std::string(env) != "0";
+    if (pair) {
+      g.tiles_m = static_cast<int>((m + 255) / 256);
+      g.total_units = pair_tiles * g.nchunks;
+      CUtensorMap tmb2 = make_slice_map(ctx, slB, kp, n, sb, 128);
+      OZ_CUDA(launch_gemm_i8_pair(&tma, &tmb2, g, ctx->num_sms, st, &launches));
+    } else {
+      g.total_units = static_cast<int>(tiles * g.nchunks);
+      OZ_CUDA(launch_gemm_i8(&tma, &tmb, g, ctx->num_sms, st, &launches));
+    }
     if (ctx->timing) OZ_CUDA(cudaEventRecord(ev[2], st));
 
     CombineArgs c{};
@@ -468,8 +482,8 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
     c.cin = dcin;
     c.ldcin = ldcin;
     if (p.strategy == 2) {
-      OZ_CUDA(launch_combine_exact(c, exact_words(cp.diagonals, t, cp.chunks.size()), st,
-                                   &launches));
+      OZ_CUDA(launch_combine_exact(c, exact_words(cp.diagonals, t, cp.chunks.size()),
+                                   cp.chunks.data(), st, &launches));
     } else {
       psi_dev = static_cast<int*>(ctx->psi.get(sizeof(int)));
       OZ_CUDA(cudaMemsetAsync(psi_dev, 0, sizeof(int), st));

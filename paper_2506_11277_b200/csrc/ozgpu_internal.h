@@ -83,9 +83,12 @@ cudaError_t launch_slice_cols(const double* b, int64_t ldb, int64_t k, int64_t n
                               cudaStream_t st, int64_t* launches);
 cudaError_t launch_gemm_i8(const CUtensorMap* tma, const CUtensorMap* tmb, const GemmArgs& args,
                            int num_sms, cudaStream_t st, int64_t* launches);
+cudaError_t launch_gemm_i8_pair(const CUtensorMap* tma, const CUtensorMap* tmb,
+                                const GemmArgs& args, int num_sms, cudaStream_t st,
+                                int64_t* launches);
 int gemm_smem_bytes();
-cudaError_t launch_combine_exact(const CombineArgs& args, int words, cudaStream_t st,
-                                 int64_t* launches);
+cudaError_t launch_combine_exact(const CombineArgs& args, int words, const ChunkDesc* host_chunks,
+                                 cudaStream_t st, int64_t* launches);
 cudaError_t launch_combine_sequential(const CombineArgs& args, cudaStream_t st,
                                       int64_t* launches);
 cudaError_t launch_row_profile(const double* a, int64_t lda, int64_t m, int64_t k,

@@ -40,6 +40,74 @@ __global__ void __launch_bounds__(256) combine_exact_kernel(const CombineArgs p)
   }
 }
 
+// Vectorised exact combine: 4 consecutive columns per thread (int4 plane
+// loads, chunk loads issued ahead of the multi-word adds), chunk shifts in
+// the parameter space.  Used when n % 4 == 0 and nchunks <= 64.
+struct ShiftTable {
+  int shift[64];
+};
+
+template <int W>
+__global__ void __launch_bounds__(256) combine_exact_v4_kernel(const CombineArgs p,
+                                                               const ShiftTable sh) {
+  const int64_t groups_per_row = p.n / 4;
+  const int64_t total = static_cast<int64_t>(p.m) * groups_per_row;
+  const bool vec_c = (p.ldc & 1) == 0 && (reinterpret_cast<uintptr_t>(p.c) & 15) == 0;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = idx / groups_per_row, j = (idx - i * groups_per_row) * 4;
+    uint64_t v[4][W];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+#pragma unroll
+      for (int w = 0; w < W; ++w) v[e][w] = 0;
+    const int4* src = reinterpret_cast<const int4*>(p.planes + i * p.ldp + j);
+    const int64_t stride4 = p.plane_stride / 4;
+    int c = 0;
+    for (; c + 4 <= p.nchunks; c += 4) {
+      int4 s[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) s[u] = __ldcs(src + (c + u) * stride4);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int shf = sh.shift[c + u];
+        words_add_shifted<W>(v[0], s[u].x, shf);
+        words_add_shifted<W>(v[1], s[u].y, shf);
+        words_add_shifted<W>(v[2], s[u].z, shf);
+        words_add_shifted<W>(v[3], s[u].w, shf);
+      }
+    }
+    for (; c < p.nchunks; ++c) {
+      const int4 s = __ldcs(src + c * stride4);
+      const int shf = sh.shift[c];
+      words_add_shifted<W>(v[0], s.x, shf);
+      words_add_shifted<W>(v[1], s.y, shf);
+      words_add_shifted<W>(v[2], s.z, shf);
+      words_add_shifted<W>(v[3], s.w, shf);
+    }
+    const long qi = static_cast<long>(__ldg(p.qa + i)) + p.w_last;
+    const int4 qb = __ldg(reinterpret_cast<const int4*>(p.qb + j));
+    double r[4];
+    r[0] = round_words<W>(v[0], qi + qb.x);
+    r[1] = round_words<W>(v[1], qi + qb.y);
+    r[2] = round_words<W>(v[2], qi + qb.z);
+    r[3] = round_words<W>(v[3], qi + qb.w);
+    if (p.axpby) {  // two roundings, no FMA contraction (scheme.cpp:369-370)
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        r[e] = __dadd_rn(__dmul_rn(p.alpha, r[e]), __dmul_rn(p.beta, p.cin[i * p.ldcin + j + e]));
+    }
+    double* dst = p.c + i * p.ldc + j;
+    if (vec_c) {
+      __stcs(reinterpret_cast<double2*>(dst), make_double2(r[0], r[1]));
+      __stcs(reinterpret_cast<double2*>(dst) + 1, make_double2(r[2], r[3]));
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) dst[e] = r[e];
+    }
+  }
+}
+
 // Sequential FP64 accumulation in the reference order (d ascending, l
 // ascending) with the TwoSum inexact counter (scheme.cpp:173-215).
 __global__ void __launch_bounds__(256) combine_sequential_kernel(const CombineArgs p) {
@@ -212,10 +280,21 @@ static inline int grid_for(int64_t work, int per_block, int cap = 148 * 16) {
 }
 
 
-cudaError_t launch_combine_exact(const CombineArgs& args, int words, cudaStream_t st,
-                                 int64_t* launches) {
+cudaError_t launch_combine_exact(const CombineArgs& args, int words, const ChunkDesc* host_chunks,
+                                 cudaStream_t st, int64_t* launches) {
   int64_t total = static_cast<int64_t>(args.m) * args.n;
   if (total == 0) return cudaSuccess;
+  if (args.n % 4 == 0 && args.nchunks <= 64 && args.ldp % 4 == 0 && words <= 3) {
+    ShiftTable sh{};
+    for (int c = 0; c < args.nchunks; ++c) sh.shift[c] = host_chunks[c].shift;
+    const int grid = grid_for(total / 4, 256, 148 * 8);
+    if (words == 2)
+      combine_exact_v4_kernel<2><<<grid, 256, 0, st>>>(args, sh);
+    else
+      combine_exact_v4_kernel<3><<<grid, 256, 0, st>>>(args, sh);
+    ++*launches;
+    return cudaGetLastError();
+  }
   int grid = grid_for(total, 256);
   switch (words) {
     case 2: combine_exact_kernel<2><<<grid, 256, 0, st>>>(args); break;

@@ -232,18 +232,19 @@ def test_native_kernels_launched(oz):
     assert oz.kernel_launches() - before >= 4
 
 
-@pytest.mark.parametrize("mode", ["fused", "split"])
-def test_epilogue_modes_match_reference(oz, ref, mode, monkeypatch):
-    """Both GEMM epilogues (fused exact-integer RMW / split planes + combine)
-    are bit-exact, incl. ragged tiles and 3-word exact values."""
+@pytest.mark.parametrize("mode,pair", [("fused", "0"), ("split", "1"), ("split", "0")])
+def test_gemm_variants_match_reference(oz, ref, mode, pair, monkeypatch):
+    """Every GEMM variant -- fused exact-integer epilogue, split planes +
+    combine on the CTA-pair (cta_group::2) kernel and on the 1-CTA kernel --
+    is bit-exact, incl. ragged tiles and 3-word exact values."""
     monkeypatch.setenv("OZGPU_EPILOGUE", mode)
+    monkeypatch.setenv("OZGPU_CTA_PAIR", pair)
     rng = np.random.default_rng(77)
     cfg = oz.MmaConfig.int8_int32()
-    for (m, k, n) in [(128, 256, 256), (300, 500, 700), (1000, 128, 513)]:
+    for (m, k, n) in [(128, 256, 256), (300, 500, 700), (520, 128, 260)]:
         a = uniform(m, k, rng)
         b = random_matrix(k, n, rng, -30, 30, 0.02)
-        for (sa, sb), sched in [((4, 4), 1), ((8, 8), 1), ((13, 12), 1), ((16, 17), 1),
-                                ((6, 7), 0)]:
+        for (sa, sb), sched in [((4, 4), 1), ((13, 12), 1), ((16, 17), 1), ((6, 7), 0)]:
             plan = oz.make_plan(cfg, k, sa, sb, oz.ScheduleKind(sched))
             got = oz.multiply(a, b, cfg, plan).c
             want, _ = ref.ref_multiply(a, b, sa, sb, sched)
