@@ -54,7 +54,7 @@ struct TileCoord {
 // Grouped rasterisation: consecutive tiles walk 8 tile-rows at a time so
 // concurrently running CTAs share A and B slice panels in L2.
 __device__ __forceinline__ TileCoord decode_tile(int t, const GemmArgs& p) {
-  const int G = 8;
+  const int G = p.group > 0 ? p.group : 8;
   const int group_size = G * p.tiles_n;
   const int group = t / group_size;
   const int first_m = group * G;
@@ -120,8 +120,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer ----------------
+  if (warp == 0) {
+    // ---------------- TMA producer (warp-wide loop, one elected issuer) ----------------
     int stage = 0;
     uint32_t phase = 0;
     for (int unit = blockIdx.x; unit < p.total_units; unit += gridDim.x) {
@@ -135,11 +135,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const int h = cd.d + 2 - l;
           for (int kb = 0; kb < p.kblocks; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
-            mbar_expect_tx(&full[stage], kStageBytes);
-            tma_load_3d(sA + stage * kABytes, &tma, &full[stage], kb * kBlockK, tc.tm * kBlockM,
-                        l - 1);
-            tma_load_3d(sB + stage * kBBytes, &tmb, &full[stage], kb * kBlockK, tc.tn * kBN,
-                        h - 1);
+            if (elect_one()) {
+              mbar_expect_tx(&full[stage], kStageBytes);
+              tma_load_3d(sA + stage * kABytes, &tma, &full[stage], kb * kBlockK,
+                          tc.tm * kBlockM, l - 1);
+              tma_load_3d(sB + stage * kBBytes, &tmb, &full[stage], kb * kBlockK, tc.tn * kBN,
+                          h - 1);
+            }
+            __syncwarp();
             if (++stage == kStages) {
               stage = 0;
               phase ^= 1;
@@ -148,9 +151,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer (single thread) ----------------
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (warp-wide loop, one elected issuer) ----------------
     constexpr uint32_t idesc = idesc_i8<kBlockM, kBN>();
+    const uint64_t ad0 = sdesc_sw128(smem_addr(sA));
+    const uint64_t bd0 = sdesc_sw128(smem_addr(sB));
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
@@ -169,18 +174,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int i = 0; i < total; ++i) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint64_t ad = sdesc_sw128(smem_addr(sA + stage * kABytes));
-          const uint64_t bd = sdesc_sw128(smem_addr(sB + stage * kBBytes));
+          if (elect_one()) {
+            // descriptor start addresses advance in 16-byte units
+            const uint64_t ad = ad0 + static_cast<uint64_t>(stage * (kABytes >> 4));
+            const uint64_t bd = bd0 + static_cast<uint64_t>(stage * (kBBytes >> 4));
 #pragma unroll
-          for (int kk = 0; kk < kBlockK / 32; ++kk)
-            tc_mma_i8(tmem_d, ad + 2 * kk, bd + 2 * kk, idesc, (i | kk) != 0);
-          tc_commit(&empty[stage]);
+            for (int kk = 0; kk < kBlockK / 32; ++kk)
+              tc_mma_i8(tmem_d, ad + 2 * kk, bd + 2 * kk, idesc, (i | kk) != 0);
+            tc_commit(&empty[stage]);
+            if (i == total - 1) tc_commit(&tfull[acc]);
+          }
+          __syncwarp();
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(&tfull[acc]);
       }
     }
   } else if (warp >= 4) {
@@ -343,8 +352,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const uint32_t tmem_base = *tmem_holder;
   const int tiles = p.tiles_m * p.tiles_n;
 
-  if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer (both CTAs) ----------------
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs; warp-wide loop, elected issuer) ----------------
+    const uint32_t full_leader0 = map_to_rank(&full[0], 0);
     int stage = 0;
     uint32_t phase = 0;
     for (int unit = pair; unit < p.total_units; unit += npairs) {
@@ -358,10 +368,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         const int h = cd.d + 2 - l;
         for (int kb = 0; kb < p.kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if (leader) mbar_expect_tx(&full[stage], 2 * kPairStageBytes);
-          const uint32_t bar = map_to_rank(&full[stage], 0);
-          tma_load_3d_pair(sA + stage * kPairHalfBytes, &tma, bar, kb * kBlockK, arow, l - 1);
-          tma_load_3d_pair(sB + stage * kPairHalfBytes, &tmb, bar, kb * kBlockK, brow, h - 1);
+          if (elect_one()) {
+            if (leader) mbar_expect_tx(&full[stage], 2 * kPairStageBytes);
+            const uint32_t bar = full_leader0 + 8 * stage;
+            tma_load_3d_pair(sA + stage * kPairHalfBytes, &tma, bar, kb * kBlockK, arow, l - 1);
+            tma_load_3d_pair(sB + stage * kPairHalfBytes, &tmb, bar, kb * kBlockK, brow, h - 1);
+          }
+          __syncwarp();
           if (++stage == kPairStages) {
             stage = 0;
             phase ^= 1;
@@ -369,9 +382,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         }
       }
     }
-  } else if (warp == 1 && lane == 0 && leader) {
-    // ---------------- MMA issuer (leader CTA, single thread) ----------------
+  } else if (warp == 1 && leader) {
+    // ---------------- MMA issuer (leader CTA; warp-wide loop, elected issuer) ----------------
     constexpr uint32_t idesc = idesc_i8<256, kBN>();
+    const uint64_t ad0 = sdesc_sw128(smem_addr(sA));
+    const uint64_t bd0 = sdesc_sw128(smem_addr(sB));
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
@@ -387,18 +402,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       for (int i = 0; i < total; ++i) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const uint64_t ad = sdesc_sw128(smem_addr(sA + stage * kPairHalfBytes));
-        const uint64_t bd = sdesc_sw128(smem_addr(sB + stage * kPairHalfBytes));
+        if (elect_one()) {
+          const uint64_t ad = ad0 + static_cast<uint64_t>(stage * (kPairHalfBytes >> 4));
+          const uint64_t bd = bd0 + static_cast<uint64_t>(stage * (kPairHalfBytes >> 4));
 #pragma unroll
-        for (int kk = 0; kk < kBlockK / 32; ++kk)
-          tc_mma_i8_pair(tmem_d, ad + 2 * kk, bd + 2 * kk, idesc, (i | kk) != 0);
-        tc_commit_pair(&empty[stage]);
+          for (int kk = 0; kk < kBlockK / 32; ++kk)
+            tc_mma_i8_pair(tmem_d, ad + 2 * kk, bd + 2 * kk, idesc, (i | kk) != 0);
+          tc_commit_pair(&empty[stage]);
+          if (i == total - 1) tc_commit_pair(&tfull[acc]);
+        }
+        __syncwarp();
         if (++stage == kPairStages) {
           stage = 0;
           phase ^= 1;
         }
       }
-      tc_commit_pair(&tfull[acc]);
     }
   } else if (warp >= 4) {
     // ---------------- epilogue (both CTAs): TMEM -> int32 chunk plane ----------------

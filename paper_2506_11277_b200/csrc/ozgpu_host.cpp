@@ -412,6 +412,7 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
     g.kblocks = static_cast<int>(kp / kBlockK);
     g.tiles_m = tiles_m;
     g.tiles_n = tiles_n;
+    if (const char* env = std::getenv("OZGPU_RASTER_G")) g.group = std::atoi(env);
     if (fused) {
       g.total_units = static_cast<int>(tiles);
       g.fused_words = words;

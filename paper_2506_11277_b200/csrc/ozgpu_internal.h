@@ -33,6 +33,7 @@ struct GemmArgs {
   int kblocks;        // kp / kBlockK
   int tiles_m, tiles_n;
   int total_units;    // tiles_m * tiles_n * nchunks (split mode)
+  int group;          // rasterisation: tile-rows per group (0 = 8)
   int32_t* planes;    // [nchunks][m][ldp] int32 chunk sums
   int64_t plane_stride;
   int64_t ldp;
