@@ -108,6 +108,75 @@ __global__ void __launch_bounds__(256) combine_exact_v4_kernel(const CombineArgs
   }
 }
 
+// Horner form of the exact combine for values that fit 127 bits:
+// V = (...((S_0 << t) + S_1) << t ...) + S_{D-1}, with S_d the int64 sum of
+// diagonal d's chunk planes (chunks are stored diagonal-major).  One 128-bit
+// shift-add per diagonal instead of a multi-word add per chunk.
+struct DiagTable {
+  int first_chunk[65];  // chunks of diagonal d: [first_chunk[d], first_chunk[d + 1])
+};
+
+__global__ void __launch_bounds__(256) combine_horner_v4_kernel(const CombineArgs p,
+                                                                const DiagTable dt) {
+  const int64_t groups_per_row = p.n / 4;
+  const int64_t total = static_cast<int64_t>(p.m) * groups_per_row;
+  const bool vec_c = (p.ldc & 1) == 0 && (reinterpret_cast<uintptr_t>(p.c) & 15) == 0;
+  const int64_t stride4 = p.plane_stride / 4;
+  const int t = p.width;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = idx / groups_per_row, j = (idx - i * groups_per_row) * 4;
+    const int4* src = reinterpret_cast<const int4*>(p.planes + i * p.ldp + j);
+    unsigned __int128 v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+    for (int d = 0; d < p.diagonals; ++d) {
+      long long s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+      for (int c = dt.first_chunk[d]; c < dt.first_chunk[d + 1]; ++c) {
+        const int4 s = __ldcs(src + c * stride4);
+        s0 += s.x;
+        s1 += s.y;
+        s2 += s.z;
+        s3 += s.w;
+      }
+      v0 = (v0 << t) + static_cast<unsigned __int128>(static_cast<__int128>(s0));
+      v1 = (v1 << t) + static_cast<unsigned __int128>(static_cast<__int128>(s1));
+      v2 = (v2 << t) + static_cast<unsigned __int128>(static_cast<__int128>(s2));
+      v3 = (v3 << t) + static_cast<unsigned __int128>(static_cast<__int128>(s3));
+    }
+    const long qi = static_cast<long>(__ldg(p.qa + i)) + p.w_last;
+    const int4 qb = __ldg(reinterpret_cast<const int4*>(p.qb + j));
+    double r[4];
+    {
+      uint64_t w[2] = {static_cast<uint64_t>(v0), static_cast<uint64_t>(v0 >> 64)};
+      r[0] = round_words<2>(w, qi + qb.x);
+    }
+    {
+      uint64_t w[2] = {static_cast<uint64_t>(v1), static_cast<uint64_t>(v1 >> 64)};
+      r[1] = round_words<2>(w, qi + qb.y);
+    }
+    {
+      uint64_t w[2] = {static_cast<uint64_t>(v2), static_cast<uint64_t>(v2 >> 64)};
+      r[2] = round_words<2>(w, qi + qb.z);
+    }
+    {
+      uint64_t w[2] = {static_cast<uint64_t>(v3), static_cast<uint64_t>(v3 >> 64)};
+      r[3] = round_words<2>(w, qi + qb.w);
+    }
+    if (p.axpby) {  // two roundings, no FMA contraction (scheme.cpp:369-370)
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        r[e] = __dadd_rn(__dmul_rn(p.alpha, r[e]), __dmul_rn(p.beta, p.cin[i * p.ldcin + j + e]));
+    }
+    double* dst = p.c + i * p.ldc + j;
+    if (vec_c) {
+      __stcs(reinterpret_cast<double2*>(dst), make_double2(r[0], r[1]));
+      __stcs(reinterpret_cast<double2*>(dst) + 1, make_double2(r[2], r[3]));
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) dst[e] = r[e];
+    }
+  }
+}
+
 // Sequential FP64 accumulation in the reference order (d ascending, l
 // ascending) with the TwoSum inexact counter (scheme.cpp:173-215).
 __global__ void __launch_bounds__(256) combine_sequential_kernel(const CombineArgs p) {
@@ -284,6 +353,25 @@ cudaError_t launch_combine_exact(const CombineArgs& args, int words, const Chunk
                                  cudaStream_t st, int64_t* launches) {
   int64_t total = static_cast<int64_t>(args.m) * args.n;
   if (total == 0) return cudaSuccess;
+  if (args.n % 4 == 0 && args.ldp % 4 == 0 && words == 2 && args.diagonals <= 64 &&
+      static_cast<int64_t>(args.diagonals - 1) * args.width + 40 <= 126) {
+    // chunks are stored diagonal-major (build_chunks): tabulate each diagonal's range
+    DiagTable dt{};
+    int c = 0;
+    for (int d = 0; d <= args.diagonals; ++d) {
+      while (c < args.nchunks && host_chunks[c].d < d) ++c;
+      dt.first_chunk[d] = c;
+    }
+    dt.first_chunk[args.diagonals] = args.nchunks;
+    bool sorted = true;
+    for (int q = 1; q < args.nchunks; ++q) sorted &= host_chunks[q - 1].d <= host_chunks[q].d;
+    if (sorted) {
+      const int grid = grid_for(total / 4, 256, 148 * 8);
+      combine_horner_v4_kernel<<<grid, 256, 0, st>>>(args, dt);
+      ++*launches;
+      return cudaGetLastError();
+    }
+  }
   if (args.n % 4 == 0 && args.nchunks <= 64 && args.ldp % 4 == 0 && words <= 3) {
     ShiftTable sh{};
     for (int c = 0; c < args.nchunks; ++c) sh.shift[c] = host_chunks[c].shift;
