@@ -445,11 +445,13 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
     g.planes = planes;
     g.plane_stride = plane;
     g.ldp = ldp;
-    // CTA-pair (cta_group::2, 256 x 256 tiles) unless the problem is too
-    // short in m or too small to fill the pairs (OZGPU_CTA_PAIR=0/1 forces).
+    // 1-CTA 128 x 256 tiles by default.  The CTA-pair kernel (cta_group::2,
+    // 256 x 256 tiles) is opt-in (OZGPU_CTA_PAIR=1): measured on B200 at
+    // 8192^3 (12,12) it issues ~2.5x the L2 misses of the 1-CTA kernel
+    // (203 GB vs 81 GB DRAM reads) and is 13-20% slower under the power cap.
     const int pair_tiles = static_cast<int>(((m + 255) / 256) * tiles_n);
-    bool pair = m >= 256 && static_cast<int64_t>(pair_tiles) * g.nchunks >= ctx->num_sms / 2;
-    if (const char* env = std::getenv("OZGPU_CTA_PAIR")) pair = std::string(env) != "0";
+    bool pair = false;
+    if (const char* env = std::getenv("OZGPU_CTA_PAIR")) pair = std::string(env) == "1" && m >= 256;
     if (pair) {
       g.tiles_m = static_cast<int>((m + 255) / 256);
       g.total_units = pair_tiles * g.nchunks;
