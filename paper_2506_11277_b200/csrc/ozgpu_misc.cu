@@ -145,22 +145,10 @@ __global__ void __launch_bounds__(256) combine_horner_v4_kernel(const CombineArg
     const long qi = static_cast<long>(__ldg(p.qa + i)) + p.w_last;
     const int4 qb = __ldg(reinterpret_cast<const int4*>(p.qb + j));
     double r[4];
-    {
-      uint64_t w[2] = {static_cast<uint64_t>(v0), static_cast<uint64_t>(v0 >> 64)};
-      r[0] = round_words<2>(w, qi + qb.x);
-    }
-    {
-      uint64_t w[2] = {static_cast<uint64_t>(v1), static_cast<uint64_t>(v1 >> 64)};
-      r[1] = round_words<2>(w, qi + qb.y);
-    }
-    {
-      uint64_t w[2] = {static_cast<uint64_t>(v2), static_cast<uint64_t>(v2 >> 64)};
-      r[2] = round_words<2>(w, qi + qb.z);
-    }
-    {
-      uint64_t w[2] = {static_cast<uint64_t>(v3), static_cast<uint64_t>(v3 >> 64)};
-      r[3] = round_words<2>(w, qi + qb.w);
-    }
+    r[0] = round_i128(v0, qi + qb.x);
+    r[1] = round_i128(v1, qi + qb.y);
+    r[2] = round_i128(v2, qi + qb.z);
+    r[3] = round_i128(v3, qi + qb.w);
     if (p.axpby) {  // two roundings, no FMA contraction (scheme.cpp:369-370)
 #pragma unroll
       for (int e = 0; e < 4; ++e)

@@ -243,4 +243,35 @@ OZ_HD double round_words(const uint64_t (&v)[W], long e) {
   return neg ? -d : d;
 }
 
+// round_words<2> specialised for a signed 128-bit value (the Horner combine):
+// same result, roughly a third of the instructions.
+OZ_HD double round_i128(unsigned __int128 v, long e) {
+  const bool neg = static_cast<int64_t>(static_cast<uint64_t>(v >> 64)) < 0;
+  if (neg) v = ~v + 1;
+  const uint64_t hi = static_cast<uint64_t>(v >> 64), lo = static_cast<uint64_t>(v);
+  if ((hi | lo) == 0) return 0.0;
+  const int nbits = hi ? 128 - clz64(hi) : 64 - clz64(lo);
+  uint64_t low;
+  if (nbits > 55) {
+    const int drop = nbits - 55;
+    low = static_cast<uint64_t>(v >> drop);
+    const bool sticky = (v << (128 - drop)) != 0;
+    e += drop;
+    if (sticky) low |= 1;  // round-to-odd at 55 bits == the reference's +1 on even
+  } else {
+    low = lo;
+  }
+  // |value| = low * 2^e with low < 2^55: convert (RN-even) then scale; the
+  // common case (normal result) is a plain exponent add.
+  const double d = u64_to_double_rn(low);
+  const uint64_t bits = dbl_bits(d);
+  const long ne = static_cast<long>(bits >> 52) + e;
+  double r;
+  if (ne >= 1 && ne <= 2046)
+    r = bits_dbl((bits & 0x800FFFFFFFFFFFFFULL) | (static_cast<uint64_t>(ne) << 52));
+  else
+    r = ldexp_rn(d, e);
+  return neg ? -r : r;
+}
+
 }  // namespace ozgpu

@@ -297,6 +297,98 @@ __global__ void __launch_bounds__(256) slice_rows_fast_kernel(
   }
 }
 
+// Two-kernel row path (no dependence between the row reduction and the
+// slice stores, so both kernels stream at HBM rate): rowmax_kernel computes
+// the block scales (one warp per row, 16-byte loads), slice_rows_stream_kernel
+// then slices 8 consecutive entries per thread over the whole matrix.
+template <bool VEC>
+__global__ void __launch_bounds__(256) rowmax_kernel(const double* __restrict__ a, int64_t lda,
+                                                     int64_t m, int64_t k,
+                                                     int* __restrict__ scales,
+                                                     int* __restrict__ status) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       row < m; row += warps) {
+    const double* ar = a + row * lda;
+    unsigned long long mx = 0;
+    int bad = 0;
+    int64_t j = 0;
+    if (VEC) {
+      const double2* a2 = reinterpret_cast<const double2*>(ar);
+      const int64_t k2 = k / 2;
+      int64_t u = lane;
+      for (; u + 96 < k2; u += 128) {
+        double2 x[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) x[q] = __ldcs(a2 + u + 32 * q);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          bad |= dirty(x[q].x) | dirty(x[q].y);
+          const unsigned long long b0 = abs_bits(x[q].x), b1 = abs_bits(x[q].y);
+          mx = b0 > mx ? b0 : mx;
+          mx = b1 > mx ? b1 : mx;
+        }
+      }
+      for (; u < k2; u += 32) {
+        const double2 x = __ldcs(a2 + u);
+        bad |= dirty(x.x) | dirty(x.y);
+        const unsigned long long b0 = abs_bits(x.x), b1 = abs_bits(x.y);
+        mx = b0 > mx ? b0 : mx;
+        mx = b1 > mx ? b1 : mx;
+      }
+      j = 2 * k2 + lane;
+    } else {
+      j = lane;
+    }
+    for (; j < k; j += 32) {
+      const double x = __ldcs(ar + j);
+      bad |= dirty(x);
+      const unsigned long long b = abs_bits(x);
+      mx = b > mx ? b : mx;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const unsigned long long t = __shfl_xor_sync(0xFFFFFFFFu, mx, o);
+      mx = t > mx ? t : mx;
+    }
+    bad = __reduce_or_sync(0xFFFFFFFFu, bad);
+    if (lane == 0) {
+      if (bad) atomicOr(status, bad);
+      scales[row] = scale_from_maxbits(mx);
+    }
+  }
+}
+
+template <int T, bool VEC>
+__global__ void __launch_bounds__(256) slice_rows_stream_kernel(
+    const double* __restrict__ a, int64_t lda, int64_t m, int64_t k, int64_t kp, int count,
+    const int* __restrict__ scales, int8_t* __restrict__ out) {
+  const int64_t groups = kp / 8;
+  const int64_t total = m * groups;
+  const int64_t plane = m * kp;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = idx / groups, g = idx - row * groups;
+    const double* ar = a + row * lda;
+    const int64_t j0 = g * 8;
+    double v[8];
+    if (VEC && j0 + 8 <= k) {
+      const double2* p2 = reinterpret_cast<const double2*>(ar + j0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double2 t2 = __ldcs(p2 + u);
+        v[2 * u] = t2.x;
+        v[2 * u + 1] = t2.y;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] = j0 + e < k ? __ldcs(ar + j0 + e) : 0.0;
+    }
+    emit8_trunc_i8<T>(v, __ldg(scales + row), count, out, plane, row * kp + j0);
+  }
+}
+
 // 128 (k) x 32 (n) tile transpose-and-slice into K-major [l][n][kp] int8.
 // Smem holds the tile column-major in 16-byte units with an XOR swizzle so
 // both the row-wise fill and the 8-entry column reads are conflict-light.
@@ -351,13 +443,17 @@ template <int T>
 static void launch_rows_fast_t(const double* a, int64_t lda, int64_t m, int64_t k, int64_t kp,
                                int count, int8_t* out, int* scales, int* status, cudaStream_t st) {
   const bool vec = (reinterpret_cast<uintptr_t>(a) & 15) == 0 && (lda & 1) == 0;
-  const int grid = grid_for(m, 8, 148 * 8);
-  if (vec)
-    slice_rows_fast_kernel<T, true><<<grid, 256, 0, st>>>(a, lda, m, k, kp, count, out, scales,
-                                                          status);
-  else
-    slice_rows_fast_kernel<T, false><<<grid, 256, 0, st>>>(a, lda, m, k, kp, count, out, scales,
-                                                           status);
+  const int grid = grid_for(m, 8, 148 * 16);
+  const int grid2 = grid_for(m * (kp / 8), 256, 148 * 16);
+  if (vec) {
+    rowmax_kernel<true><<<grid, 256, 0, st>>>(a, lda, m, k, scales, status);
+    slice_rows_stream_kernel<T, true><<<grid2, 256, 0, st>>>(a, lda, m, k, kp, count, scales,
+                                                             out);
+  } else {
+    rowmax_kernel<false><<<grid, 256, 0, st>>>(a, lda, m, k, scales, status);
+    slice_rows_stream_kernel<T, false><<<grid2, 256, 0, st>>>(a, lda, m, k, kp, count, scales,
+                                                              out);
+  }
 }
 
 template <int T>
@@ -383,7 +479,7 @@ cudaError_t launch_slice_rows(const double* a, int64_t lda, int64_t m, int64_t k
       case 2: launch_rows_fast_t<2>(a, lda, m, k, kp, count, o, scales, status, st); break;
       default: launch_rows_fast_t<1>(a, lda, m, k, kp, count, o, scales, status, st); break;
     }
-    ++*launches;
+    *launches += 2;  // rowmax + stream slicing
     return cudaGetLastError();
   }
   int grid = static_cast<int>(m < 148 * 32 ? m : 148 * 32);

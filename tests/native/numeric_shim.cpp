@@ -37,3 +37,8 @@ void nt_slices(double x, int q, int width, int count, int mode, long long* out) 
   for (int l = 0; l < count; ++l) out[l] = slice_of(e, l, width, count, mode);
 }
 }
+
+extern "C" double nt_round_i128(uint64_t lo, uint64_t hi, long e) {
+  unsigned __int128 v = (static_cast<unsigned __int128>(hi) << 64) | lo;
+  return round_i128(v, e);
+}

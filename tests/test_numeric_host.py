@@ -123,3 +123,21 @@ def test_slice_fields_match_oracle(nt, po, mode):
             for j in range(40):
                 nt.nt_slices(x[i, j], int(sc[i]), width, count, mode, out.ctypes.data)
                 assert np.array_equal(out, sl[:, i, j]), (i, j)
+
+
+def test_round_i128_matches_bigints(nt):
+    nt.nt_round_i128.restype = ctypes.c_double
+    nt.nt_round_i128.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_long]
+    rng = np.random.default_rng(6)
+    for trial in range(20000):
+        bits = int(rng.integers(1, 127))
+        v = int(rng.integers(0, 2**62)) << max(0, bits - 62)
+        v |= int(rng.integers(0, 2**20)) if trial % 3 else 0
+        v &= (1 << 126) - 1
+        if trial % 2:
+            v = -v
+        e = int(rng.integers(-1250, 950))
+        u = v % (1 << 128)
+        got = nt.nt_round_i128(u & ((1 << 64) - 1), u >> 64, e)
+        want = _exact_round(v, e)
+        assert got == want or (math.isinf(got) and math.isinf(want)), (v, e, got, want)
