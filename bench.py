@@ -191,7 +191,10 @@ def reference_arm(args, cfg_key):
     cfg = CONFIGS[cfg_key]
     line = {"metric": METRIC, "unit": "TFLOP/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": "int8",
+            "data": "synthetic: reference generator random_uniform(-0.5,0.5) seeds 1,2"
+                    if cfg["gen"] == "uniform" else
+                    "synthetic: reference gen_kappa_d(2^60, seed 7, rotate)",
             "config": {"workload": cfg["name"], "m": cfg["m"], "n": cfg["n"], "k": cfg["k"]}}
     if not pyoracle.have_ref():
         line["unavailable"] = "oracle/_ref/libozref.so not built"
@@ -214,17 +217,18 @@ def reference_arm(args, cfg_key):
     if cfg["m"] * cfg["n"] <= 1024 * 1024 and cfg["k"] <= 1024:
         bs = 64
     blocks = cpu_blocks(cfg["m"], cfg["n"], threads, bs)
-    rates = []
+    rates, walls = [], []
     for s in range(args.warmup + args.steps):
         _, secs = run_cpu_reference(a, b, slices, blocks, threads)
         flops = sum(2.0 * (r1 - r0) * (c1 - c0) * cfg["k"] for r0, r1, c0, c1 in blocks)
         if s >= args.warmup:
             rates.append(flops / secs / 1e12)
+            walls.append(secs)
     value = statistics.mean(rates)
     sample = (f"{len(blocks)} C blocks of {bs}x{bs} with full k={cfg['k']} per step, reference "
               f"multiply() (oracle/_ref, compiled from the reference sources) on {threads} "
               f"host threads; rate = sampled FP64-equiv flops / wall time")
-    line.update({"value": value, "ms_per_step": None,
+    line.update({"value": value, "ms_per_step": 1e3 * statistics.mean(walls),
                  "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads,
                                   "kind": "reference", "sample": sample},
                  "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
