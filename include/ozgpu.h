@@ -149,6 +149,19 @@ int ozgpu_select_slices(double kappa_a, double kappa_b, int width, double u, int
 int ozgpu_scaling_profile(ozgpu_ctx* ctx, int64_t m, int64_t k, int64_t n, const double* a,
                           int64_t lda, const double* b, int64_t ldb, ozgpu_profile* out);
 
+/* block_ratios, proj/src/analysis.cpp:25-47, on the GPU: per-row
+ * (orientation 0) or per-column (1) max / min-nonzero magnitude, 1.0 for an
+ * all-zero block; *has_zero_block set when one exists.  ratios_out has rows
+ * (orientation 0) or cols (1) entries. */
+int ozgpu_block_ratios(ozgpu_ctx* ctx, int orientation, int64_t rows, int64_t cols,
+                       const double* x, int64_t ldx, double* ratios_out, int* has_zero_block);
+/* abs_product / gemm_reference, proj/src/matrix.cpp:31-54, on the GPU:
+ * out(i,j) = sum_r op(a_ir) op(b_rj) in binary64, r ascending, zero a_ir
+ * skipped, op = |.| when absolute != 0 (identical rounding sequence). */
+int ozgpu_fp64_gemm(ozgpu_ctx* ctx, int absolute, int64_t m, int64_t k, int64_t n,
+                    const double* a, int64_t lda, const double* b, int64_t ldb, double* out,
+                    int64_t ldo);
+
 /* ---- the GEMM (multiply, proj/src/scheme.cpp:219-361) ------------------ */
 /* Host buffers: A m x k (lda), B k x n (ldb), C m x n (ldc), all row-major
  * binary64.  Copies in, runs slicing + int8 tcgen05 pair GEMMs + exact

@@ -521,10 +521,20 @@ void d2h(double* dst, int64_t ld, const void* src, int64_t rows, int64_t cols, c
 
 void check_plan(const ozgpu_plan* plan) {
   if (!plan) throw std::invalid_argument("multiply: null plan");
-  if (plan->slices_a < 1 || plan->slices_b < 1)
-    throw std::invalid_argument("split: need at least one slice");
   if (plan->strategy < 0 || plan->strategy > 2)
     throw std::invalid_argument("multiply: unknown accumulation strategy");
+}
+
+// Errors the reference raises from split() after multiply's own validation
+// (slicing.cpp:69-72), plus the int8 operand limit of the tensor-core path.
+std::string plan_error(const ozgpu_plan& p) {
+  if (p.width < 1 || p.width > 62) return "split: width out of range";
+  if (p.slices_a < 1 || p.slices_b < 1) return "split: need at least one slice";
+  if (p.mode == 1 && p.width < 2) return "split: nearest mode needs width >= 2";
+  if (p.width > 7)
+    return "multiply: slice width " + std::to_string(p.width) +
+           " exceeds the int8 tensor-core operand (t <= 7)";
+  return {};
 }
 
 // Host-pointer multiply / multiply_axpby.
@@ -540,8 +550,10 @@ void host_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double
   double* db = static_cast<double*>(ctx->in_b.get(sizeof(double) * k * n + 8));
   h2d(da, a, m, k, lda, st);
   h2d(db, b, k, n, ldb, st);
-  if (k < 1 || v.capacity_error || v.precision_error) {
-    // the clean-input check precedes these errors (scheme.cpp:223-239)
+  const std::string perr = plan_error(p);
+  if (k < 1 || v.capacity_error || v.precision_error || !perr.empty()) {
+    // the clean-input check precedes these errors (scheme.cpp:223-239, then
+    // split()'s argument checks, slicing.cpp:69-72)
     int* status = static_cast<int*>(ctx->status.get(sizeof(int)));
     OZ_CUDA(cudaMemsetAsync(status, 0, sizeof(int), st));
     int64_t launches = 0;
@@ -562,7 +574,8 @@ void host_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double
     ctx->launches += launches;
     if (hs) throw std::invalid_argument("multiply: inputs must be finite with no negative zeros");
     if (k < 1) throw std::invalid_argument("multiply: empty inner dimension");
-    throw std::domain_error(v.message);
+    if (v.capacity_error || v.precision_error) throw std::domain_error(v.message);
+    throw std::invalid_argument(perr);
   }
   double* dc = static_cast<double*>(ctx->io_c.get(sizeof(double) * m * n + 8));
   const double* dcin = nullptr;
@@ -809,6 +822,76 @@ int ozgpu_scaling_profile(ozgpu_ctx* ctx, int64_t m, int64_t k, int64_t n, const
   });
 }
 
+int ozgpu_block_ratios(ozgpu_ctx* ctx, int orientation, int64_t rows, int64_t cols,
+                       const double* x, int64_t ldx, double* ratios_out, int* has_zero_block) {
+  return guarded([&] {
+    if (!ctx || !ratios_out || !has_zero_block)
+      throw std::invalid_argument("block_ratios: null argument");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    OZ_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    int64_t launches = 0;
+    double* dx = static_cast<double*>(ctx->in_a.get(sizeof(double) * rows * cols + 8));
+    h2d(dx, x, rows, cols, ldx, st);
+    *has_zero_block = 0;
+    if (orientation == 0) {
+      double* ratios = static_cast<double*>(ctx->ratios.get(sizeof(double) * (rows + 1)));
+      int* zf = static_cast<int*>(ctx->status.get(sizeof(int)));
+      OZ_CUDA(cudaMemsetAsync(zf, 0, sizeof(int), st));
+      OZ_CUDA(launch_row_profile(dx, cols, rows, cols, ratios, zf, st, &launches));
+      if (rows)
+        OZ_CUDA(cudaMemcpyAsync(ratios_out, ratios, sizeof(double) * rows, cudaMemcpyDeviceToHost,
+                                st));
+      OZ_CUDA(cudaMemcpyAsync(has_zero_block, zf, sizeof(int), cudaMemcpyDeviceToHost, st));
+      OZ_CUDA(cudaStreamSynchronize(st));
+    } else {
+      auto* cmax = static_cast<unsigned long long*>(ctx->colmax.get(8 * (cols + 1)));
+      auto* cmin = static_cast<unsigned long long*>(ctx->colmin.get(8 * (cols + 1)));
+      OZ_CUDA(launch_col_profile(dx, cols, rows, cols, cmax, cmin, st, &launches));
+      std::vector<unsigned long long> hmax(cols), hmin(cols);
+      if (cols) {
+        OZ_CUDA(cudaMemcpyAsync(hmax.data(), cmax, 8 * cols, cudaMemcpyDeviceToHost, st));
+        OZ_CUDA(cudaMemcpyAsync(hmin.data(), cmin, 8 * cols, cudaMemcpyDeviceToHost, st));
+      }
+      OZ_CUDA(cudaStreamSynchronize(st));
+      for (int64_t j = 0; j < cols; ++j) {
+        if (hmax[j] == 0) {
+          ratios_out[j] = 1.0;
+          *has_zero_block = 1;
+          continue;
+        }
+        double mx, mn;
+        std::memcpy(&mx, &hmax[j], 8);
+        std::memcpy(&mn, &hmin[j], 8);
+        ratios_out[j] = mx / mn;
+      }
+    }
+    ctx->launches += launches;
+  });
+}
+
+int ozgpu_fp64_gemm(ozgpu_ctx* ctx, int absolute, int64_t m, int64_t k, int64_t n,
+                    const double* a, int64_t lda, const double* b, int64_t ldb, double* out,
+                    int64_t ldo) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("fp64_gemm: null context");
+    if (m < 0 || n < 0 || k < 0) throw std::invalid_argument("fp64_gemm: shape mismatch");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    OZ_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    int64_t launches = 0;
+    double* da = static_cast<double*>(ctx->in_a.get(sizeof(double) * m * k + 8));
+    double* db = static_cast<double*>(ctx->in_b.get(sizeof(double) * k * n + 8));
+    double* dc = static_cast<double*>(ctx->io_c.get(sizeof(double) * m * n + 8));
+    h2d(da, a, m, k, lda, st);
+    h2d(db, b, k, n, ldb, st);
+    OZ_CUDA(launch_fp64_gemm(absolute, m, k, n, da, k, db, n, dc, n, st, &launches));
+    d2h(out, ldo, dc, m, n, st);
+    OZ_CUDA(cudaStreamSynchronize(st));
+    ctx->launches += launches;
+  });
+}
+
 int ozgpu_dgemm(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda,
                 const double* b, int64_t ldb, double* c, int64_t ldc, ozgpu_mma_config cfg,
                 const ozgpu_plan* plan, ozgpu_diag* diag) {
@@ -845,6 +928,8 @@ int ozgpu_dgemm_device(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const do
     if (k < 1) throw std::invalid_argument("multiply: empty inner dimension");
     ValidationResult v = host_validation(cfg, *plan, k);
     if (v.capacity_error || v.precision_error) throw std::domain_error(v.message);
+    const std::string perr = plan_error(*plan);
+    if (!perr.empty()) throw std::invalid_argument(perr);
     std::lock_guard<std::mutex> lock(ctx->mu);
     OZ_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t st = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream

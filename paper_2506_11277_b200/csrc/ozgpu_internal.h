@@ -98,6 +98,9 @@ cudaError_t launch_row_profile(const double* a, int64_t lda, int64_t m, int64_t 
 cudaError_t launch_col_profile(const double* b, int64_t ldb, int64_t k, int64_t n,
                                unsigned long long* colmax, unsigned long long* colmin,
                                cudaStream_t st, int64_t* launches);
+cudaError_t launch_fp64_gemm(int absolute, int64_t m, int64_t k, int64_t n, const double* a,
+                             int64_t lda, const double* b, int64_t ldb, double* out, int64_t ldo,
+                             cudaStream_t st, int64_t* launches);
 cudaError_t launch_pack_i8(const int64_t* x, int64_t rows, int64_t cols, int transpose,
                            int64_t kp, int8_t* out, cudaStream_t st, int64_t* launches);
 cudaError_t launch_integer_gemm_exact(const int64_t* x, const int64_t* y, const int64_t* c,

@@ -201,6 +201,41 @@ __global__ void __launch_bounds__(256) combine_sequential_kernel(const CombineAr
   if (local_max) atomicMax(p.realized_psi, local_max);
 }
 
+// abs_product / gemm_reference (matrix.cpp:31-54): one thread per output,
+// r ascending, zero a_ir skipped, separate multiply and add roundings.
+__global__ void __launch_bounds__(256) fp64_gemm_kernel(int absolute, int64_t m, int64_t k,
+                                                        int64_t n, const double* __restrict__ a,
+                                                        int64_t lda, const double* __restrict__ b,
+                                                        int64_t ldb, double* __restrict__ out,
+                                                        int64_t ldo) {
+  const int64_t total = m * n;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = idx / n, j = idx - i * n;
+    double acc = 0.0;
+    for (int64_t r = 0; r < k; ++r) {
+      double ar = __ldg(a + i * lda + r);
+      if (absolute) ar = fabs(ar);
+      if (ar == 0.0) continue;
+      double br = __ldg(b + r * ldb + j);
+      if (absolute) br = fabs(br);
+      acc = __dadd_rn(acc, __dmul_rn(ar, br));
+    }
+    out[i * ldo + j] = acc;
+  }
+}
+
+cudaError_t launch_fp64_gemm(int absolute, int64_t m, int64_t k, int64_t n, const double* a,
+                             int64_t lda, const double* b, int64_t ldb, double* out, int64_t ldo,
+                             cudaStream_t st, int64_t* launches) {
+  if (m * n == 0) return cudaSuccess;
+  int64_t g = (m * n + 255) / 256;
+  fp64_gemm_kernel<<<static_cast<int>(g < 148 * 16 ? g : 148 * 16), 256, 0, st>>>(
+      absolute, m, k, n, a, lda, b, ldb, out, ldo);
+  ++*launches;
+  return cudaGetLastError();
+}
+
 // ----------------------------------------------------------------------------
 // kappa profile (analysis.cpp:25-47): per-row / per-column max and min
 // nonzero magnitude.
