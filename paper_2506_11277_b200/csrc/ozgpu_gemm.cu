@@ -66,26 +66,122 @@ __device__ __forceinline__ TileCoord decode_tile(int t, const GemmArgs& p) {
   return c;
 }
 
-// Work unit -> (tile, first chunk, chunk count).
+// Work unit -> (tile, first chunk, chunk count, linear tile index).
 __device__ __forceinline__ void decode_unit(int unit, const GemmArgs& p, bool fused,
-                                            TileCoord& tc, int& c0, int& nc) {
+                                            TileCoord& tc, int& c0, int& nc, int& tile) {
   if (fused) {
+    tile = unit;
     tc = decode_tile(unit, p);
     c0 = 0;
     nc = p.nchunks;
   } else {
     const int tiles = p.tiles_m * p.tiles_n;
-    c0 = unit / tiles;
+    const int pos = unit / tiles;
+    c0 = p.proc_order ? __ldg(p.proc_order + pos) : pos;
     nc = 1;
-    tc = decode_tile(unit - c0 * tiles, p);
+    tile = unit - pos * tiles;
+    tc = decode_tile(tile, p);
   }
+}
+__device__ __forceinline__ void decode_unit(int unit, const GemmArgs& p, bool fused,
+                                            TileCoord& tc, int& c0, int& nc) {
+  int tile;
+  decode_unit(unit, p, fused, tc, c0, nc, tile);
+}
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* ptr) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void epilogue_bar() {  // the 4 epilogue warps only
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+
+// Final-chunk epilogue of the split+final mode: for one 32-column slab of the
+// warp's 32 rows, sum every chunk of the tile diagonal by diagonal (the final
+// chunk from TMEM registers, the others from their int32 planes), Horner-
+// accumulate V = V * 2^t + S_d in 128 bits, round once (round_i128) and stage
+// the doubles for a row-coalesced store.
+__device__ __forceinline__ void final_combine_slab(const GemmArgs& p, const uint32_t (&r)[32],
+                                                   int row, int col0, long qrow, int lane,
+                                                   double* stage_w) {
+  const int qcol = col0 + lane < p.n ? __ldg(p.qb + col0 + lane) : 0;
+  const bool row_ok = row < p.m;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const int cb = col0 + half * 16;
+    const bool full16 = cb + 16 <= p.n;
+    unsigned __int128 v[16];
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) v[jj] = 0;
+    for (int d = 0; d < p.diagonals; ++d) {
+      long long s[16];
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) s[jj] = 0;
+      const int c_end = __ldg(p.diag_first + d + 1);
+      for (int c = __ldg(p.diag_first + d); c < c_end; ++c) {
+        if (c == p.final_chunk) {
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) s[jj] += static_cast<int32_t>(r[half * 16 + jj]);
+        } else if (row_ok) {
+          const int32_t* src = p.planes + static_cast<int64_t>(c) * p.plane_stride +
+                               static_cast<int64_t>(row) * p.ldp + cb;
+          if (full16) {
+            const int4* s4 = reinterpret_cast<const int4*>(src);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int4 x = __ldcg(s4 + u);
+              s[4 * u] += x.x;
+              s[4 * u + 1] += x.y;
+              s[4 * u + 2] += x.z;
+              s[4 * u + 3] += x.w;
+            }
+          } else {
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj)
+              if (cb + jj < p.n) s[jj] += __ldcg(src + jj);
+          }
+        }
+      }
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj)
+        v[jj] = (v[jj] << p.width) + static_cast<unsigned __int128>(static_cast<__int128>(s[jj]));
+    }
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) {
+      const int j = half * 16 + jj;
+      const int qj = __shfl_sync(0xFFFFFFFFu, qcol, j);
+      stage_w[lane * 32 + (j ^ lane)] = round_i128(v[jj], qrow + qj + p.w_last);
+    }
+  }
+}
+
+// Row-coalesced store of a staged 32x32 block of C (optionally D = a*C + b*Cin).
+__device__ __forceinline__ void store_staged(const GemmArgs& p, const double* stage_w, int row0,
+                                             int col0, int lane) {
+  __syncwarp();
+  const int col = col0 + lane;
+#pragma unroll 4
+  for (int rr = 0; rr < 32; ++rr) {
+    const int orow = row0 + rr;
+    double d = stage_w[rr * 32 + (lane ^ rr)];
+    if (orow < p.m && col < p.n) {
+      if (p.axpby)
+        d = __dadd_rn(__dmul_rn(p.alpha, d),
+                      __dmul_rn(p.beta, p.cin[static_cast<int64_t>(orow) * p.ldcin + col]));
+      p.c[static_cast<int64_t>(orow) * p.ldc + col] = d;
+    }
+  }
+  __syncwarp();
 }
 
 template <int W>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_i8_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
                    const GemmArgs p) {
-  constexpr bool kFused = W > 0;
+  constexpr bool kFused = W >= 2;
+  constexpr bool kFinal = W == 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -202,19 +298,34 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int it = 0;
     for (int unit = blockIdx.x; unit < p.total_units; unit += gridDim.x) {
       TileCoord tc;
-      int c0, nc;
-      decode_unit(unit, p, kFused, tc, c0, nc);
+      int c0, nc, tile;
+      decode_unit(unit, p, kFused, tc, c0, nc, tile);
       const int row0 = tc.tm * kBlockM + q * 32;
       const int row = row0 + lane;
       long qrow = 0;
-      if constexpr (kFused) qrow = row < p.m ? __ldg(p.qa + row) : 0;
+      if constexpr (kFused || kFinal) qrow = row < p.m ? __ldg(p.qa + row) : 0;
       for (int c = c0; c < c0 + nc; ++c, ++it) {
         const int acc = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
         mbar_wait(&tfull[acc], aphase);
         tc_fence_after();
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * kBN;
-        if constexpr (!kFused) {
+        if (kFinal && c == p.final_chunk) {
+          // every other chunk of this tile must have stored its plane
+          if (threadIdx.x == 128) {
+            while (ld_acquire_gpu(p.tile_counters + tile) < p.nchunks - 1) __nanosleep(200);
+            __threadfence();
+          }
+          epilogue_bar();
+#pragma unroll 1
+          for (int s0 = 0; s0 < kBN; s0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(taddr + s0, r);
+            const int col0 = tc.tn * kBN + s0;
+            final_combine_slab(p, r, row, col0, qrow, lane, stage_w);
+            store_staged(p, stage_w, row0, col0, lane);
+          }
+        } else if constexpr (!kFused) {
           int32_t* dst = p.planes + static_cast<int64_t>(c) * p.plane_stride +
                          static_cast<int64_t>(row) * p.ldp;
 #pragma unroll 1
@@ -233,6 +344,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                   if (col0 + v < p.n) dst[col0 + v] = static_cast<int32_t>(r[v]);
               }
             }
+          }
+          if constexpr (kFinal) {
+            // publish this chunk of the tile (release: fence by every writer,
+            // then one counter increment after the epilogue barrier)
+            __threadfence();
+            epilogue_bar();
+            if (threadIdx.x == 128) atomicAdd(p.tile_counters + tile, 1);
           }
         } else {
           const bool first = c == 0, last = c == p.nchunks - 1;
@@ -262,22 +380,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 stage_w[lane * 32 + (j ^ lane)] = d;
               }
             }
-            if (last) {
-              __syncwarp();
-              const int col = col0 + lane;
-#pragma unroll 4
-              for (int rr = 0; rr < 32; ++rr) {
-                const int orow = row0 + rr;
-                double d = stage_w[rr * 32 + (lane ^ rr)];
-                if (orow < p.m && col < p.n) {
-                  if (p.axpby)
-                    d = __dadd_rn(__dmul_rn(p.alpha, d),
-                                  __dmul_rn(p.beta, p.cin[static_cast<int64_t>(orow) * p.ldcin + col]));
-                  p.c[static_cast<int64_t>(orow) * p.ldc + col] = d;
-                }
-              }
-              __syncwarp();
-            }
+            if (last) store_staged(p, stage_w, row0, col0, lane);
           }
         }
         tc_fence_before();
@@ -506,6 +609,7 @@ cudaError_t launch_gemm_i8(const CUtensorMap* tma, const CUtensorMap* tmb, const
   cudaError_t e;
   switch (args.fused_words) {
     case 0: e = launch_t<0>(tma, tmb, args, grid, kSmemSplit, st); break;
+    case 1: e = launch_t<1>(tma, tmb, args, grid, kSmemFused, st); break;
     case 2: e = launch_t<2>(tma, tmb, args, grid, kSmemFused, st); break;
     case 3: e = launch_t<3>(tma, tmb, args, grid, kSmemFused, st); break;
     default: return cudaErrorInvalidValue;

@@ -110,6 +110,8 @@ struct ozgpu_ctx {
   ozgpu::DevBuf slices_a, slices_b, qa, qb, colmax, colmin, status, planes, chunks, psi, scratch;
   ozgpu::DevBuf in_a, in_b, io_c, in_c2, ratios, i64a, i64b, i64c, i64o, ovf;
   std::vector<ozgpu::ChunkDesc> host_chunks;
+  std::vector<int> host_aux;
+  ozgpu::DevBuf aux, counters;
   // stage timing (ozgpu_set_stage_timing)
   bool timing = false;
   std::vector<std::array<cudaEvent_t, 4>> pending_events;
@@ -459,6 +461,58 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
       OZ_CUDA(launch_gemm_i8_pair(&tma, &tmb2, g, ctx->num_sms, st, &launches));
     } else {
       g.total_units = static_cast<int>(tiles * g.nchunks);
+      // Exact combine folded into the GEMM: the largest chunk runs last and
+      // its epilogue sums the tile's other planes (Horner, 128-bit) -- needs
+      // the exact value to fit 127 bits and >= 2 chunks.
+      bool final_mode = p.strategy == 2 && g.nchunks >= 2 && cp.diagonals <= 64 &&
+                        static_cast<int64_t>(cp.diagonals - 1) * t + 40 <= 126;
+      if (const char* env = std::getenv("OZGPU_EPILOGUE"))
+        if (std::string(env) == "split") final_mode = false;
+      if (final_mode) {
+        int fin = 0;
+        for (int c = 1; c < g.nchunks; ++c)
+          if (cp.chunks[c].npairs >= cp.chunks[fin].npairs) fin = c;
+        std::vector<int>& aux = ctx->host_aux;
+        aux.clear();
+        for (int c = 0; c < g.nchunks; ++c)
+          if (c != fin) aux.push_back(c);
+        aux.push_back(fin);
+        int cc = 0;
+        for (int d = 0; d <= cp.diagonals; ++d) {
+          while (cc < g.nchunks && cp.chunks[cc].d < d) ++cc;
+          aux.push_back(d == cp.diagonals ? g.nchunks : cc);
+        }
+        int* daux = static_cast<int*>(ctx->aux.get(sizeof(int) * aux.size()));
+        OZ_CUDA(cudaMemcpyAsync(daux, aux.data(), sizeof(int) * aux.size(),
+                                cudaMemcpyHostToDevice, st));
+        int* counters = static_cast<int*>(ctx->counters.get(sizeof(int) * tiles));
+        OZ_CUDA(cudaMemsetAsync(counters, 0, sizeof(int) * tiles, st));
+        g.proc_order = daux;
+        g.diag_first = daux + g.nchunks;
+        g.final_chunk = fin;
+        g.tile_counters = counters;
+        g.diagonals = cp.diagonals;
+        g.width = t;
+        g.fused_words = 1;
+        g.qa = qa;
+        g.qb = qb;
+        g.w_last = w_last;
+        g.c = dc;
+        g.ldc = ldc;
+        g.axpby = axpby ? 1 : 0;
+        g.alpha = alpha;
+        g.beta = beta;
+        g.cin = dcin;
+        g.ldcin = ldcin;
+        OZ_CUDA(launch_gemm_i8(&tma, &tmb, g, ctx->num_sms, st, &launches));
+        if (ctx->timing) {
+          OZ_CUDA(cudaEventRecord(ev[2], st));
+          OZ_CUDA(cudaEventRecord(ev[3], st));
+          ctx->pending_events.push_back(ev);
+        }
+        ctx->launches += launches;
+        return nullptr;
+      }
       OZ_CUDA(launch_gemm_i8(&tma, &tmb, g, ctx->num_sms, st, &launches));
     }
     if (ctx->timing) OZ_CUDA(cudaEventRecord(ev[2], st));

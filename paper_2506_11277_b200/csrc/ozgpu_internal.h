@@ -37,7 +37,18 @@ struct GemmArgs {
   int32_t* planes;    // [nchunks][m][ldp] int32 chunk sums
   int64_t plane_stride;
   int64_t ldp;
-  // fused exact epilogue (fused_words = W > 0; units are tiles)
+  // split mode with the exact combine folded into the last chunk's epilogue
+  // (fused_words == 1): units run chunk-major in proc_order; the final
+  // chunk's epilogue waits on tile_counters[tile] == nchunks - 1, then sums
+  // the other chunks' planes diagonal by diagonal (diag_first) Horner-style,
+  // rounds and stores C
+  const int* proc_order;   // position -> chunk id (null = identity)
+  int final_chunk;
+  int* tile_counters;
+  const int* diag_first;   // diagonals + 1 entries
+  int diagonals;
+  int width;
+  // fused exact epilogue (fused_words = W >= 2; units are tiles)
   int fused_words;
   uint64_t* scratch;  // per CTA: W x 256 x 128 words
   const int* qa;
