@@ -257,3 +257,59 @@ def test_gemm_variants_match_reference(oz, ref, mode, pair, monkeypatch):
     got = oz.multiply_axpby(1.5, a, b, -0.25, c, cfg, plan).c
     want = ref.ref_multiply_axpby(1.5, a, b, -0.25, c, 7, 7)
     assert bits_equal(got, want)
+
+
+@pytest.mark.parametrize("k,slices", [(20000, (12, 12)), (70000, (6, 5)), (131072, (3, 3))])
+def test_long_k_multi_chunk_diagonals(oz, ref, k, slices):
+    """k large enough that a diagonal's int32 capacity holds fewer pairs than
+    the diagonal has (cap = floor((2^31-1) / (k 127^2)): 8 at k=20000, 1 at
+    k >= 65536), so diagonals split into several chunks."""
+    rng = np.random.default_rng(k)
+    m, n = 24, 20
+    a = uniform(m, k, rng)
+    b = random_matrix(k, n, rng, -3, 3, 0.01)
+    cfg = oz.MmaConfig.int8_int32()
+    plan = oz.make_plan(cfg, k, *slices)
+    got = oz.multiply(a, b, cfg, plan)
+    blocks = [(0, 12, 0, 10), (0, 12, 10, 20), (12, 24, 0, 10), (12, 24, 10, 20)]
+    want, _ = ref.ref_multiply_blocks(a, b, slices[0], slices[1], blocks, 4)
+    assert bits_equal(got.c, want), mismatch_report(got.c, want)
+
+
+def test_concurrent_callers_are_safe(oz, ref):
+    """multiply is called from host thread pools in the reference CLI
+    (main.cpp:422,486,557); results must stay bitwise deterministic."""
+    import concurrent.futures as cf
+    rng = np.random.default_rng(99)
+    cfg = oz.MmaConfig.int8_int32()
+    cases = []
+    for i in range(12):
+        m, k, n = (int(v) for v in rng.integers(8, 200, size=3))
+        a, b = uniform(m, k, rng), uniform(k, n, rng)
+        cases.append((a, b, oz.make_plan(cfg, k, 4 + i % 5, 3 + i % 4)))
+    want = [oz.multiply(a, b, cfg, p).c for a, b, p in cases]
+    with cf.ThreadPoolExecutor(8) as ex:
+        got = list(ex.map(lambda c: oz.multiply(c[0], c[1], cfg, c[2]).c, cases * 3))
+    for i, g in enumerate(got):
+        assert bits_equal(g, want[i % len(cases)])
+
+
+def test_large_shape_sampled_blocks(oz, ref):
+    """A 2304 x 4096 x 2176 product (ragged vs the 128 x 256 tiles) with the
+    estimator's slices: sampled 32 x 32 blocks equal the reference's (blocking
+    is exact)."""
+    m, k, n = 2304, 4096, 2176
+    a = oz.random_uniform(m, k, 1, -0.5, 0.5)
+    b = oz.random_uniform(k, n, 2, -0.5, 0.5)
+    cfg = oz.MmaConfig.int8_int32()
+    prof = oz.scaling_profile(a, b)
+    t = oz.optimal_slice_width(cfg, k)
+    sel = oz.select_slices(prof.kappa_a, prof.kappa_b, t, 2.0 ** -53, 24,
+                           oz.SelectOptions(target=1e-15, acc_bits_used=2 * t + 12))
+    plan = oz.make_plan(cfg, k, sel.slices_a, sel.slices_b)
+    c = oz.multiply(a, b, cfg, plan).c
+    blocks = [(r, r + 32, q, q + 32) for r, q in [(0, 0), (2272, 2144), (1000, 517), (128, 2000),
+                                                  (2200, 64), (640, 1280), (1500, 1500), (32, 31)]]
+    want, _ = ref.ref_multiply_blocks(a, b, sel.slices_a, sel.slices_b, blocks, 8)
+    for r0, r1, c0, c1 in blocks:
+        assert bits_equal(c[r0:r1, c0:c1], want[r0:r1, c0:c1]), (r0, c0)
