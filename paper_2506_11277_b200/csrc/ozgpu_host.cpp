@@ -112,6 +112,9 @@ struct ozgpu_ctx {
   std::vector<ozgpu::ChunkDesc> host_chunks;
   std::vector<int> host_aux;
   ozgpu::DevBuf aux, counters;
+  // row-blocked H2D / compute / D2H pipeline of ozgpu_dgemm
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  cudaEvent_t pipe_events[10] = {};
   // stage timing (ozgpu_set_stage_timing)
   bool timing = false;
   std::vector<std::array<cudaEvent_t, 4>> pending_events;
@@ -337,7 +340,9 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
                   const double* db, int64_t ldb, double* dc, int64_t ldc,
                   const ozgpu_mma_config& cfg, const ozgpu_plan& p, cudaStream_t st,
                   int* dev_status, bool axpby, double alpha, double beta, const double* dcin,
-                  int64_t ldcin) {
+                  int64_t ldcin, bool reuse_b = false) {
+  // reuse_b: B's slices / scales / status from the previous call on this
+  // stream are still valid (row-blocked pipeline of host_multiply)
   int64_t launches = 0;
   std::array<cudaEvent_t, 4> ev{};
   if (ctx->timing) {
@@ -360,11 +365,12 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
   int* qb = static_cast<int*>(ctx->qb.get(sizeof(int) * (n + 1)));
   auto* colmax = static_cast<unsigned long long*>(ctx->colmax.get(8 * (n + 1)));
   int* status = dev_status ? dev_status : static_cast<int*>(ctx->status.get(sizeof(int)));
-  OZ_CUDA(cudaMemsetAsync(status, 0, sizeof(int), st));
+  if (!reuse_b) OZ_CUDA(cudaMemsetAsync(status, 0, sizeof(int), st));
 
   OZ_CUDA(launch_slice_rows(da, lda, m, k, kp, t, sa, p.mode, slA, 0, qa, status, st, &launches));
-  OZ_CUDA(launch_slice_cols(db, ldb, k, n, kp, t, sb, p.mode, slB, 0, qb, colmax, status, st,
-                            &launches));
+  if (!reuse_b)
+    OZ_CUDA(launch_slice_cols(db, ldb, k, n, kp, t, sb, p.mode, slB, 0, qb, colmax, status, st,
+                              &launches));
   if (ctx->timing) OZ_CUDA(cudaEventRecord(ev[1], st));
 
   int* psi_dev = nullptr;
@@ -602,10 +608,56 @@ void host_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double
   ValidationResult v = host_validation(cfg, p, k);
   double* da = static_cast<double*>(ctx->in_a.get(sizeof(double) * m * k + 8));
   double* db = static_cast<double*>(ctx->in_b.get(sizeof(double) * k * n + 8));
+  const std::string perr = plan_error(p);
+  const bool failing = k < 1 || v.capacity_error || v.precision_error || !perr.empty();
+  // Row-blocked pipeline for large products: B goes over PCIe first and is
+  // sliced once; A arrives in row blocks on a copy stream, each block is
+  // sliced + multiplied on the compute stream as soon as it lands, and its C
+  // rows go back on a third stream while the next block computes.
+  const int64_t bytes = 8 * (m * k + k * n + m * n);
+  const int nblk = (!failing && !axpby && p.strategy == 2 && m >= 2048 && bytes >= (64 << 20))
+                       ? 4 : 1;
+  if (nblk > 1) {
+    if (!ctx->h2d_stream) {
+      OZ_CUDA(cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
+      OZ_CUDA(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
+      for (auto& e : ctx->pipe_events) OZ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    cudaEvent_t* ev = ctx->pipe_events;  // [0] B in, [1..4] A blocks in, [5..8] C blocks out
+    double* dc = static_cast<double*>(ctx->io_c.get(sizeof(double) * m * n + 8));
+    OZ_CUDA(cudaEventRecord(ev[9], st));  // order after earlier work on the compute stream
+    OZ_CUDA(cudaStreamWaitEvent(ctx->h2d_stream, ev[9], 0));
+    h2d(db, b, k, n, ldb, ctx->h2d_stream);
+    OZ_CUDA(cudaEventRecord(ev[0], ctx->h2d_stream));
+    const int64_t rows = round_up((m + nblk - 1) / nblk, 128);
+    for (int r = 0; r < nblk; ++r) {
+      const int64_t r0 = std::min(m, r * rows), r1 = std::min(m, r0 + rows);
+      h2d(da + r0 * k, a + r0 * lda, r1 - r0, k, lda, ctx->h2d_stream);
+      OZ_CUDA(cudaEventRecord(ev[1 + r], ctx->h2d_stream));
+    }
+    OZ_CUDA(cudaStreamWaitEvent(st, ev[0], 0));
+    for (int r = 0; r < nblk; ++r) {
+      const int64_t r0 = std::min(m, r * rows), r1 = std::min(m, r0 + rows);
+      OZ_CUDA(cudaStreamWaitEvent(st, ev[1 + r], 0));
+      if (r1 > r0)
+        run_multiply(ctx, r1 - r0, n, k, da + r0 * k, k, db, n, dc + r0 * n, n, cfg, p, st,
+                     nullptr, false, 1.0, 0.0, nullptr, 0, /*reuse_b=*/r > 0);
+      OZ_CUDA(cudaEventRecord(ev[5 + r], st));
+      OZ_CUDA(cudaStreamWaitEvent(ctx->d2h_stream, ev[5 + r], 0));
+      d2h(c + r0 * ldc, ldc, dc + r0 * n, r1 - r0, n, ctx->d2h_stream);
+    }
+    int hs = 0;
+    OZ_CUDA(cudaMemcpyAsync(&hs, ctx->status.p, sizeof(int), cudaMemcpyDeviceToHost,
+                            ctx->d2h_stream));
+    OZ_CUDA(cudaStreamSynchronize(ctx->d2h_stream));
+    OZ_CUDA(cudaStreamSynchronize(st));
+    if (hs) throw std::invalid_argument("multiply: inputs must be finite with no negative zeros");
+    if (diag) *diag = make_diag(p, cfg, m, n, k, 0);
+    return;
+  }
   h2d(da, a, m, k, lda, st);
   h2d(db, b, k, n, ldb, st);
-  const std::string perr = plan_error(p);
-  if (k < 1 || v.capacity_error || v.precision_error || !perr.empty()) {
+  if (failing) {
     // the clean-input check precedes these errors (scheme.cpp:223-239, then
     // split()'s argument checks, slicing.cpp:69-72)
     int* status = static_cast<int*>(ctx->status.get(sizeof(int)));
@@ -737,6 +789,16 @@ int ozgpu_destroy(ozgpu_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->h2d_stream) {
+      cudaStreamSynchronize(ctx->h2d_stream);
+      cudaStreamSynchronize(ctx->d2h_stream);
+      cudaStreamDestroy(ctx->h2d_stream);
+      cudaStreamDestroy(ctx->d2h_stream);
+      for (cudaEvent_t e : ctx->pipe_events) cudaEventDestroy(e);
+    }
+    for (auto& ev : ctx->pending_events)
+      for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
     delete ctx;
   });
 }
