@@ -467,13 +467,16 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
       OZ_CUDA(launch_gemm_i8_pair(&tma, &tmb2, g, ctx->num_sms, st, &launches));
     } else {
       g.total_units = static_cast<int>(tiles * g.nchunks);
-      // Exact combine folded into the GEMM: the largest chunk runs last and
-      // its epilogue sums the tile's other planes (Horner, 128-bit) -- needs
-      // the exact value to fit 127 bits and >= 2 chunks.
-      bool final_mode = p.strategy == 2 && g.nchunks >= 2 && cp.diagonals <= 64 &&
-                        static_cast<int64_t>(cp.diagonals - 1) * t + 40 <= 126;
+      // Opt-in (OZGPU_EPILOGUE=final): the exact combine folded into the
+      // GEMM -- the largest chunk runs last and its epilogue sums the tile's
+      // other planes (Horner, 128-bit).  Bit-exact, but measured ~3% slower
+      // than split + the combine kernel under the B200 power cap (the heavy
+      // epilogue competes with the MMAs for power), so not the default.
+      bool final_mode = false;
       if (const char* env = std::getenv("OZGPU_EPILOGUE"))
-        if (std::string(env) == "split") final_mode = false;
+        final_mode = std::string(env) == "final" && p.strategy == 2 && g.nchunks >= 2 &&
+                     cp.diagonals <= 64 &&
+                     static_cast<int64_t>(cp.diagonals - 1) * t + 40 <= 126;
       if (final_mode) {
         int fin = 0;
         for (int c = 1; c < g.nchunks; ++c)

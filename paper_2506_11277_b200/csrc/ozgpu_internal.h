@@ -74,6 +74,7 @@ struct CombineArgs {
   long w_last;         // exponent of the least significant diagonal: -(D+1)t (+2 nearest)
   int width;           // t
   int diagonals;       // D
+  int hgroup;          // Horner combine: diagonals per int64 run (>= 1)
   int mode;            // 0 truncate, 1 nearest
   double* c;
   int64_t ldc;

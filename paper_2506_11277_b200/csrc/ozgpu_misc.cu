@@ -3,6 +3,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <algorithm>
 
 #include "ozgpu_internal.h"
 #include "ozgpu_numeric.h"
@@ -128,19 +129,32 @@ __global__ void __launch_bounds__(256) combine_horner_v4_kernel(const CombineArg
     const int64_t i = idx / groups_per_row, j = (idx - i * groups_per_row) * 4;
     const int4* src = reinterpret_cast<const int4*>(p.planes + i * p.ldp + j);
     unsigned __int128 v0 = 0, v1 = 0, v2 = 0, v3 = 0;
-    for (int d = 0; d < p.diagonals; ++d) {
-      long long s0 = 0, s1 = 0, s2 = 0, s3 = 0;
-      for (int c = dt.first_chunk[d]; c < dt.first_chunk[d + 1]; ++c) {
-        const int4 s = __ldcs(src + c * stride4);
-        s0 += s.x;
-        s1 += s.y;
-        s2 += s.z;
-        s3 += s.w;
+    // Diagonals in runs of p.hgroup: a run is Horner-summed in int64 (the
+    // multiply-by-2^t runs on the FMA pipe; the host sizes the run so it
+    // cannot overflow), then folded into the 128-bit value with one shift-add.
+    const long long radix = 1LL << t;
+    for (int d0 = 0; d0 < p.diagonals; d0 += p.hgroup) {
+      const int d1 = min(p.diagonals, d0 + p.hgroup);
+      long long a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+      for (int d = d0; d < d1; ++d) {
+        long long s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+        for (int c = dt.first_chunk[d]; c < dt.first_chunk[d + 1]; ++c) {
+          const int4 s = __ldcs(src + c * stride4);
+          s0 += s.x;
+          s1 += s.y;
+          s2 += s.z;
+          s3 += s.w;
+        }
+        a0 = a0 * radix + s0;
+        a1 = a1 * radix + s1;
+        a2 = a2 * radix + s2;
+        a3 = a3 * radix + s3;
       }
-      v0 = (v0 << t) + static_cast<unsigned __int128>(static_cast<__int128>(s0));
-      v1 = (v1 << t) + static_cast<unsigned __int128>(static_cast<__int128>(s1));
-      v2 = (v2 << t) + static_cast<unsigned __int128>(static_cast<__int128>(s2));
-      v3 = (v3 << t) + static_cast<unsigned __int128>(static_cast<__int128>(s3));
+      const int sh = t * (d1 - d0);
+      v0 = (v0 << sh) + static_cast<unsigned __int128>(static_cast<__int128>(a0));
+      v1 = (v1 << sh) + static_cast<unsigned __int128>(static_cast<__int128>(a1));
+      v2 = (v2 << sh) + static_cast<unsigned __int128>(static_cast<__int128>(a2));
+      v3 = (v3 << sh) + static_cast<unsigned __int128>(static_cast<__int128>(a3));
     }
     const long qi = static_cast<long>(__ldg(p.qa + i)) + p.w_last;
     const int4 qb = __ldg(reinterpret_cast<const int4*>(p.qb + j));
@@ -389,8 +403,17 @@ cudaError_t launch_combine_exact(const CombineArgs& args, int words, const Chunk
     bool sorted = true;
     for (int q = 1; q < args.nchunks; ++q) sorted &= host_chunks[q - 1].d <= host_chunks[q].d;
     if (sorted) {
+      // run length so an int64 Horner run cannot overflow:
+      // bits(S_d) + t (len - 1) + 1 <= 63, bits(S_d) = 31 + ceil(log2 chunks_d)
+      int maxc = 1;
+      for (int d = 0; d < args.diagonals; ++d)
+        maxc = std::max(maxc, dt.first_chunk[d + 1] - dt.first_chunk[d]);
+      int lg = 0;
+      while ((1 << lg) < maxc) ++lg;
+      CombineArgs a2 = args;
+      a2.hgroup = std::max(1, 1 + (62 - (31 + lg)) / std::max(1, args.width));
       const int grid = grid_for(total / 4, 256, 148 * 8);
-      combine_horner_v4_kernel<<<grid, 256, 0, st>>>(args, dt);
+      combine_horner_v4_kernel<<<grid, 256, 0, st>>>(a2, dt);
       ++*launches;
       return cudaGetLastError();
     }

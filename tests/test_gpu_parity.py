@@ -232,7 +232,7 @@ def test_native_kernels_launched(oz):
     assert oz.kernel_launches() - before >= 4
 
 
-@pytest.mark.parametrize("mode,pair", [("default", "0"), ("fused", "0"), ("split", "1"), ("split", "0")])
+@pytest.mark.parametrize("mode,pair", [("default", "0"), ("final", "0"), ("fused", "0"), ("split", "1")])
 def test_gemm_variants_match_reference(oz, ref, mode, pair, monkeypatch):
     """Every GEMM variant -- fused exact-integer epilogue, split planes +
     combine on the CTA-pair (cta_group::2) kernel and on the 1-CTA kernel --
