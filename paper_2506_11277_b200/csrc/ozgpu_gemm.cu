@@ -80,7 +80,16 @@ __device__ __forceinline__ void decode_unit(int unit, const GemmArgs& p, bool fu
     c0 = p.proc_order ? __ldg(p.proc_order + pos) : pos;
     nc = 1;
     tile = unit - pos * tiles;
-    tc = decode_tile(tile, p);
+    if (p.pair_order) {
+      // diagnostic: walk 256-row pair tiles (as the CTA-pair kernel does),
+      // the two 128-row halves on consecutive units / CTAs
+      GemmArgs q = p;
+      q.tiles_m = p.tiles_m / 2;
+      tc = decode_tile(tile >> 1, q);
+      tc.tm = 2 * tc.tm + (tile & 1);
+    } else {
+      tc = decode_tile(tile, p);
+    }
   }
 }
 __device__ __forceinline__ void decode_unit(int unit, const GemmArgs& p, bool fused,
