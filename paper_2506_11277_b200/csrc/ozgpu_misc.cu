@@ -179,6 +179,87 @@ __global__ void __launch_bounds__(256) combine_horner_v4_kernel(const CombineArg
   }
 }
 
+// Straight-line variant of the Horner combine: the chunk loads of a batch of
+// 16 are all issued before any arithmetic (static register indexing), and a
+// host-built program says per chunk whether it opens a new diagonal
+// (int64 run *= 2^t) or closes a run (fold into 128 bits, shift given).
+struct HornerProgram {
+  int flags[64];       // bit0: opens a new diagonal, bit1: fold the run first
+  int fold_shift[64];  // bits to shift the 128-bit value by when folding
+  int final_shift;     // fold of the last run
+};
+
+__global__ void __launch_bounds__(256) combine_horner2_v4_kernel(const CombineArgs p,
+                                                                 const HornerProgram hp) {
+  const int64_t groups_per_row = p.n / 4;
+  const int64_t total = static_cast<int64_t>(p.m) * groups_per_row;
+  const bool vec_c = (p.ldc & 1) == 0 && (reinterpret_cast<uintptr_t>(p.c) & 15) == 0;
+  const int64_t stride4 = p.plane_stride / 4;
+  const long long radix = 1LL << p.width;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = idx / groups_per_row, j = (idx - i * groups_per_row) * 4;
+    const int4* src = reinterpret_cast<const int4*>(p.planes + i * p.ldp + j);
+    unsigned __int128 v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+    long long a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    for (int cb = 0; cb < p.nchunks; cb += 16) {
+      int4 s[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (cb + u < p.nchunks) s[u] = __ldcs(src + (cb + u) * stride4);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int c = cb + u;
+        if (c < p.nchunks) {
+          const int f = hp.flags[c];
+          if (f & 2) {
+            const int sh = hp.fold_shift[c];
+            v0 = (v0 << sh) + static_cast<unsigned __int128>(static_cast<__int128>(a0));
+            v1 = (v1 << sh) + static_cast<unsigned __int128>(static_cast<__int128>(a1));
+            v2 = (v2 << sh) + static_cast<unsigned __int128>(static_cast<__int128>(a2));
+            v3 = (v3 << sh) + static_cast<unsigned __int128>(static_cast<__int128>(a3));
+            a0 = a1 = a2 = a3 = 0;
+          } else if (f & 1) {
+            a0 *= radix;
+            a1 *= radix;
+            a2 *= radix;
+            a3 *= radix;
+          }
+          a0 += s[u].x;
+          a1 += s[u].y;
+          a2 += s[u].z;
+          a3 += s[u].w;
+        }
+      }
+    }
+    const int sh = hp.final_shift;
+    v0 = (v0 << sh) + static_cast<unsigned __int128>(static_cast<__int128>(a0));
+    v1 = (v1 << sh) + static_cast<unsigned __int128>(static_cast<__int128>(a1));
+    v2 = (v2 << sh) + static_cast<unsigned __int128>(static_cast<__int128>(a2));
+    v3 = (v3 << sh) + static_cast<unsigned __int128>(static_cast<__int128>(a3));
+    const long qi = static_cast<long>(__ldg(p.qa + i)) + p.w_last;
+    const int4 qb = __ldg(reinterpret_cast<const int4*>(p.qb + j));
+    double r[4];
+    r[0] = round_i128(v0, qi + qb.x);
+    r[1] = round_i128(v1, qi + qb.y);
+    r[2] = round_i128(v2, qi + qb.z);
+    r[3] = round_i128(v3, qi + qb.w);
+    if (p.axpby) {  // two roundings, no FMA contraction (scheme.cpp:369-370)
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        r[e] = __dadd_rn(__dmul_rn(p.alpha, r[e]), __dmul_rn(p.beta, p.cin[i * p.ldcin + j + e]));
+    }
+    double* dst = p.c + i * p.ldc + j;
+    if (vec_c) {
+      __stcs(reinterpret_cast<double2*>(dst), make_double2(r[0], r[1]));
+      __stcs(reinterpret_cast<double2*>(dst) + 1, make_double2(r[2], r[3]));
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) dst[e] = r[e];
+    }
+  }
+}
+
 // Sequential FP64 accumulation in the reference order (d ascending, l
 // ascending) with the TwoSum inexact counter (scheme.cpp:173-215).
 __global__ void __launch_bounds__(256) combine_sequential_kernel(const CombineArgs p) {
@@ -413,7 +494,27 @@ cudaError_t launch_combine_exact(const CombineArgs& args, int words, const Chunk
       CombineArgs a2 = args;
       a2.hgroup = std::max(1, 1 + (62 - (31 + lg)) / std::max(1, args.width));
       const int grid = grid_for(total / 4, 256, 148 * 8);
-      combine_horner_v4_kernel<<<grid, 256, 0, st>>>(a2, dt);
+      if (args.nchunks <= 64) {
+        HornerProgram hp{};
+        int run_len = 0;
+        for (int c = 0; c < args.nchunks; ++c) {
+          const bool newdiag = c == 0 || host_chunks[c].d != host_chunks[c - 1].d;
+          if (c > 0 && newdiag) {
+            if (run_len == a2.hgroup) {
+              hp.flags[c] = 2;
+              hp.fold_shift[c] = args.width * run_len;
+              run_len = 0;
+            } else {
+              hp.flags[c] = 1;
+            }
+          }
+          if (newdiag) ++run_len;
+        }
+        hp.final_shift = args.width * run_len;
+        combine_horner2_v4_kernel<<<grid, 256, 0, st>>>(a2, hp);
+      } else {
+        combine_horner_v4_kernel<<<grid, 256, 0, st>>>(a2, dt);
+      }
       ++*launches;
       return cudaGetLastError();
     }
