@@ -152,6 +152,17 @@ void init_ctx(ozgpu_ctx* ctx, int device) {
   ctx->encode = reinterpret_cast<EncodeTiledFn>(fn);
 }
 
+// TMA L2 sector promotion of the slice loads (OZGPU_L2_PROMO=0/64/128/256).
+CUtensorMapL2promotion l2_promotion() {
+  if (const char* env = std::getenv("OZGPU_L2_PROMO")) {
+    const int v = std::atoi(env);
+    if (v == 0) return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    if (v == 64) return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    if (v == 128) return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+  }
+  return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+
 // 3-D int8 tensor map over slices [count][rows][kp], box {128, box_rows, 1},
 // 128-byte swizzle (matches the UMMA SW128 K-major descriptor).
 CUtensorMap make_slice_map(ozgpu_ctx* ctx, const void* base, int64_t kp, int64_t rows,
@@ -164,7 +175,7 @@ CUtensorMap make_slice_map(ozgpu_ctx* ctx, const void* base, int64_t kp, int64_t
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = ctx->encode(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims,
                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion(),
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw DeviceError("cuTensorMapEncodeTiled failed: " + std::to_string(r));
   return m;
