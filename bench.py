@@ -289,17 +289,10 @@ def main():
     b_d = torch.from_numpy(b_h).to(dev)
     c_d = torch.empty((m, n), dtype=torch.float64, device=dev)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
-    row_groups = col_groups = None
-    if world > 1:
-        row_groups = [dist.new_group(shard.row_group(world, i)) for i in range(pr)]
-        col_groups = [dist.new_group(shard.col_group(world, j)) for j in range(pc)]
+    xchg = shard.PanelExchange(world, rank)
 
     def step(p=plan):
-        if world > 1:
-            if pc > 1:
-                dist.broadcast(a_d, src=shard.a_owner(world, blk.i), group=row_groups[blk.i])
-            if pr > 1:
-                dist.broadcast(b_d, src=shard.b_owner(world, blk.j), group=col_groups[blk.j])
+        xchg.exchange(a_d, b_d)  # A row-panel / B column-panel from their owners (NCCL)
         oz.multiply_device(m, n, k, a_d.data_ptr(), k, b_d.data_ptr(), n, c_d.data_ptr(), n,
                            mcfg, p, stream=torch.cuda.current_stream().cuda_stream,
                            status_ptr=status.data_ptr())

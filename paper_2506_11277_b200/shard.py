@@ -71,3 +71,31 @@ def a_owner(world: int, i: int) -> int:
 
 def b_owner(world: int, j: int) -> int:
     return col_group(world, j)[0]
+
+
+class PanelExchange:
+    """The exchange step of a sharded multiply, shared by bench.py (NCCL, CUDA
+    tensors) and the gloo tests (CPU tensors): one process group per block row
+    and per block column, created collectively in the same order on every
+    rank; `exchange` broadcasts A row-panel i from rank (i, 0) along row
+    group i and B column-panel j from rank (0, j) along column group j."""
+
+    def __init__(self, world: int, rank: int):
+        import torch.distributed as dist
+        self.world, self.rank = world, rank
+        self.pr, self.pc = grid_for(world)
+        self.i, self.j = divmod(rank, self.pc)
+        self.row_groups = [dist.new_group(row_group(world, i)) for i in range(self.pr)] \
+            if world > 1 else []
+        self.col_groups = [dist.new_group(col_group(world, j)) for j in range(self.pc)] \
+            if world > 1 else []
+
+    def exchange(self, a_panel, b_panel) -> None:
+        """In place: a_panel / b_panel hold the owner's data afterwards."""
+        import torch.distributed as dist
+        if self.world == 1:
+            return
+        if self.pc > 1:
+            dist.broadcast(a_panel, src=a_owner(self.world, self.i), group=self.row_groups[self.i])
+        if self.pr > 1:
+            dist.broadcast(b_panel, src=b_owner(self.world, self.j), group=self.col_groups[self.j])

@@ -26,10 +26,8 @@ def _worker(rank, world, port, m, n, k, out_q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from oracle import pyoracle as po
-    pr, pc = shard.grid_for(world)
     blk = shard.block_of(rank, world, m, n)
-    rows = [g for g in [dist.new_group(shard.row_group(world, i)) for i in range(pr)]]
-    cols = [g for g in [dist.new_group(shard.col_group(world, j)) for j in range(pc)]]
+    xchg = shard.PanelExchange(world, rank)  # the same exchange bench.py runs over NCCL
     # panels exist only on their owners (deterministic per-panel seeds)
     a = torch.zeros(blk.row1 - blk.row0, k, dtype=torch.float64)
     b = torch.zeros(k, blk.col1 - blk.col0, dtype=torch.float64)
@@ -37,17 +35,14 @@ def _worker(rank, world, port, m, n, k, out_q):
         a.copy_(torch.from_numpy(po.port_random_uniform(m, k, 1, -0.5, 0.5)[blk.row0:blk.row1]))
     if rank == shard.b_owner(world, blk.j):
         b.copy_(torch.from_numpy(po.port_random_uniform(k, n, 2, -0.5, 0.5)[:, blk.col0:blk.col1]))
-    if pc > 1:
-        dist.broadcast(a, src=shard.a_owner(world, blk.i), group=rows[blk.i])
-    if pr > 1:
-        dist.broadcast(b, src=shard.b_owner(world, blk.j), group=cols[blk.j])
+    xchg.exchange(a, b)
     c = po.port_multiply_exact(a.numpy(), b.numpy(), 5, 4)
     out_q.put((rank, blk.row0, blk.row1, blk.col0, blk.col1, c))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_sharded_blocks_equal_monolithic(po, world):
     m, n, k = 40, 36, 50
     ctx = mp.get_context("spawn")
