@@ -483,8 +483,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           if (elect_one()) {
             if (leader) mbar_expect_tx(&full[stage], 2 * kPairStageBytes);
             const uint32_t bar = full_leader0 + 8 * stage;
-            tma_load_3d_pair(sA + stage * kPairHalfBytes, &tma, bar, kb * kBlockK, arow, l - 1);
-            tma_load_3d_pair(sB + stage * kPairHalfBytes, &tmb, bar, kb * kBlockK, brow, h - 1);
+            if (p.l2_hint) {
+              const uint64_t pol = p.l2_hint == 1 ? l2_policy_evict_last() : l2_policy_evict_normal();
+              tma_load_3d_pair_hint(sA + stage * kPairHalfBytes, &tma, bar, kb * kBlockK, arow,
+                                    l - 1, pol);
+              tma_load_3d_pair_hint(sB + stage * kPairHalfBytes, &tmb, bar, kb * kBlockK, brow,
+                                    h - 1, pol);
+            } else {
+              tma_load_3d_pair(sA + stage * kPairHalfBytes, &tma, bar, kb * kBlockK, arow, l - 1);
+              tma_load_3d_pair(sB + stage * kPairHalfBytes, &tmb, bar, kb * kBlockK, brow, h - 1);
+            }
           }
           __syncwarp();
           if (++stage == kPairStages) {

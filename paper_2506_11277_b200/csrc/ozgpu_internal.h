@@ -35,6 +35,7 @@ struct GemmArgs {
   int total_units;    // tiles_m * tiles_n * nchunks (split mode)
   int group;          // rasterisation: tile-rows per group (0 = 8)
   int pair_order;     // diagnostic: 1-CTA kernel walks 256-row pair tiles
+  int l2_hint;        // CTA-pair kernel TMA cache policy: 0 none, 1 evict_last, 2 evict_normal
   int32_t* planes;    // [nchunks][m][ldp] int32 chunk sums
   int64_t plane_stride;
   int64_t ldp;
