@@ -595,3 +595,94 @@ def stage_times(reset: bool = True, device: Optional[int] = None):
     calls = _I64()
     _check(_lib.ozgpu_stage_times(_ctx(device), ms, ctypes.byref(calls), int(reset)))
     return ms[0], ms[1], ms[2], calls.value
+
+
+# ------------------------------------------------ analysis helpers (GPU)
+
+_sig("ozgpu_block_ratios", ctypes.c_int, _P, ctypes.c_int, _I64, _I64, _DP, _I64, _DP,
+     ctypes.POINTER(ctypes.c_int))
+_sig("ozgpu_fp64_gemm", ctypes.c_int, _P, ctypes.c_int, _I64, _I64, _I64, _DP, _I64, _DP, _I64,
+     _DP, _I64)
+
+
+def block_ratios(x, orientation: BlockOrientation, device: Optional[int] = None):
+    """analysis.cpp:25-47 on the GPU -> (ratios, has_zero_block)."""
+    x = _f64(x)
+    nb = x.shape[0] if int(orientation) == 0 else x.shape[1]
+    out = np.ones(nb, dtype=np.float64)
+    z = ctypes.c_int()
+    _check(_lib.ozgpu_block_ratios(_ctx(device), int(orientation), x.shape[0], x.shape[1], _dp(x),
+                                   x.shape[1], _dp(out), ctypes.byref(z)))
+    return out, bool(z.value)
+
+
+def kappa(x, orientation: BlockOrientation, device: Optional[int] = None) -> float:
+    """analysis.cpp:51-56: 2 * max(1, worst max/min-nonzero ratio)."""
+    r, _ = block_ratios(x, orientation, device)
+    return 2.0 * max(1.0, float(r.max()) if r.size else 1.0)
+
+
+def abs_product(a, b, device: Optional[int] = None) -> np.ndarray:
+    """|A||B| in binary64 with the reference's summation order (matrix.cpp:31-41)."""
+    a, b = _f64(a), _f64(b)
+    if a.shape[1] != b.shape[0]:
+        raise InvalidArgument("abs_product: shape mismatch")
+    out = np.empty((a.shape[0], b.shape[1]))
+    _check(_lib.ozgpu_fp64_gemm(_ctx(device), 1, a.shape[0], a.shape[1], b.shape[1], _dp(a),
+                                a.shape[1], _dp(b), b.shape[1], _dp(out), b.shape[1]))
+    return out
+
+
+def zeta(kappa_a: float, kappa_b: float, slices_a: int, slices_b: int, width: int) -> float:
+    """analysis.cpp:70-77."""
+    import math
+    if not (kappa_a > 0 and kappa_b > 0):
+        raise InvalidArgument("zeta: kappas must be positive")
+    return (math.ldexp(kappa_a, -slices_a * width) + math.ldexp(kappa_b, -slices_b * width) +
+            math.ldexp(kappa_a * kappa_b, -(slices_a + slices_b) * width))
+
+
+def gamma_factor(n: int, u: float) -> float:
+    """analysis.cpp:79-84."""
+    if n < 0:
+        raise InvalidArgument("gamma_factor: n must be >= 0")
+    nu = float(n) * u
+    if nu >= 1.0:
+        raise DomainError("gamma_factor: n*u >= 1, bound is meaningless")
+    return nu / (1.0 - nu)
+
+
+@dataclass
+class ErrorReport:
+    """analysis.hpp:52-64."""
+    kappa_a: float
+    kappa_b: float
+    zeta_ab: float
+    gamma_psi: float
+    coefficient: float
+    first_order_coefficient: float
+    kind: str
+    bound: np.ndarray
+
+
+def error_bound(a, b, plan: MultiplyPlan, u: float = 2.0 ** -53,
+                device: Optional[int] = None) -> ErrorReport:
+    """analysis.cpp:86-131: coefficient * |A||B| * (1 + 8u), |A||B| on the GPU."""
+    import math
+    prof = scaling_profile(a, b, device)
+    t, sa, sb = plan.width, plan.slices_a, plan.slices_b
+    z = zeta(prof.kappa_a, prof.kappa_b, sa, sb, t)
+    g = gamma_factor(plan.psi, u)
+    if plan.schedule == ScheduleKind.FULL:
+        kind, coef = "full", z + g * (1.0 + z)
+    else:
+        if sa <= sb:
+            kind, cut = "reduced_a_le_b", math.ldexp(float(sa) * prof.kappa_a * prof.kappa_b, -sb * t)
+        else:
+            kind, cut = "reduced_a_gt_b", math.ldexp(float(sb) * prof.kappa_a * prof.kappa_b, -sa * t)
+        gn = gamma_factor(plan.psi + 1, u)
+        coef = z + cut + gn * (1.0 + z + cut)
+    first = (math.ldexp(prof.kappa_a, -sa * t) + math.ldexp(prof.kappa_b, -sb * t) +
+             float(plan.psi) * u)
+    bound = abs_product(a, b, device) * (coef * (1.0 + 8.0 * u))
+    return ErrorReport(prof.kappa_a, prof.kappa_b, z, g, coef, first, kind, bound)

@@ -313,3 +313,22 @@ def test_large_shape_sampled_blocks(oz, ref):
     want, _ = ref.ref_multiply_blocks(a, b, sel.slices_a, sel.slices_b, blocks, 8)
     for r0, r1, c0, c1 in blocks:
         assert bits_equal(c[r0:r1, c0:c1], want[r0:r1, c0:c1]), (r0, c0)
+
+
+def test_error_bound_matches_reference_and_contains(oz, ref):
+    """analysis.cpp:86-131 (|A||B| on the GPU in the reference's order): the
+    bound matrix equals the reference's bitwise and contains |C - exact|."""
+    rng = np.random.default_rng(31)
+    cfg = oz.MmaConfig.int8_int32()
+    a = random_matrix(40, 90, rng, -8, 8, 0.05)
+    b = random_matrix(90, 30, rng, -8, 8, 0.05)
+    for sa, sb, sched in [(3, 4, 1), (5, 5, 0), (6, 3, 1)]:
+        plan = oz.make_plan(cfg, 90, sa, sb, oz.ScheduleKind(sched))
+        rep = oz.error_bound(a, b, plan)
+        coef, bound = ref.ref_error_bound(a, b, sa, sb, sched)
+        assert rep.coefficient == coef
+        assert bits_equal(rep.bound, bound)
+        c = oz.multiply(a, b, cfg, plan).c
+        exact = ref.ref_exact_gemm(a, b)
+        assert (np.abs(c - exact) <= rep.bound).all()
+    assert oz.kappa(a, oz.BlockOrientation.ROWS) == ref.ref_scaling_profile(a, b)[0]
