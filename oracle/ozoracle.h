@@ -5,7 +5,7 @@
  * checker: it is never the thing measured or shipped.
  *
  * Parity is pinned: tests/test_oracle.py checks every function below against
- * the reference's golden vectors (proj/tests/*_test.cpp) and against the
+ * the reference's golden vectors (proj/tests/ *_test.cpp) and against the
  * unmodified reference compiled from its own sources (oracle/_ref/libozref.so,
  * see oracle/Makefile).
  *
