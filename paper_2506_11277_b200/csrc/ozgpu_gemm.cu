@@ -66,9 +66,39 @@ __device__ __forceinline__ TileCoord decode_tile(int t, const GemmArgs& p) {
   return c;
 }
 
-// Work unit -> (tile, first chunk, chunk count, linear tile index).
+// Chunk id at position `pos` of the unit's chunk sequence (proc_order
+// permutes chunks so each bin's chunks are contiguous; null = identity).
+__device__ __forceinline__ int chunk_at(const GemmArgs& p, int pos) {
+  return p.proc_order ? __ldg(p.proc_order + pos) : pos;
+}
+
+// Work unit -> (tile, first chunk position, chunk count, linear tile index).
+// Split mode: unit = (bin, tile), bin-major.  A bin is a run of chunks of
+// one tile (bin_first[b] .. bin_first[b+1]) whose pair counts add up to the
+// same total for every bin (host bin packing), so every CTA of a wave
+// streams the same slice pair at the same time and shares it through L2.
 __device__ __forceinline__ void decode_unit(int unit, const GemmArgs& p, bool fused,
-                                            TileCoord& tc, int& c0, int& nc, int& tile) {
+                                            TileCoord& tc, int& c0, int& nc, int& tile,
+                                            int mc_rank = -1) {
+  if (mc_rank >= 0) {
+    // 2-CTA cluster: unit = (bin, 256 x 256 super-tile); the CTA of rank r
+    // takes its 128-row half (the two share the B panel through multicast)
+    GemmArgs q = p;
+    q.tiles_m = (p.tiles_m + 1) / 2;
+    const int tiles = q.tiles_m * p.tiles_n;
+    const int pos = unit / tiles;
+    if (p.bin_first) {
+      c0 = __ldg(p.bin_first + pos);
+      nc = __ldg(p.bin_first + pos + 1) - c0;
+    } else {
+      c0 = pos;
+      nc = 1;
+    }
+    tile = unit - pos * tiles;
+    tc = decode_tile(tile, q);
+    tc.tm = 2 * tc.tm + mc_rank;
+    return;
+  }
   if (fused) {
     tile = unit;
     tc = decode_tile(unit, p);
@@ -77,8 +107,13 @@ __device__ __forceinline__ void decode_unit(int unit, const GemmArgs& p, bool fu
   } else {
     const int tiles = p.tiles_m * p.tiles_n;
     const int pos = unit / tiles;
-    c0 = p.proc_order ? __ldg(p.proc_order + pos) : pos;
-    nc = 1;
+    if (p.bin_first) {
+      c0 = __ldg(p.bin_first + pos);
+      nc = __ldg(p.bin_first + pos + 1) - c0;
+    } else {
+      c0 = pos;
+      nc = 1;
+    }
     tile = unit - pos * tiles;
     if (p.pair_order) {
       // diagnostic: walk 256-row pair tiles (as the CTA-pair kernel does),
@@ -93,9 +128,9 @@ __device__ __forceinline__ void decode_unit(int unit, const GemmArgs& p, bool fu
   }
 }
 __device__ __forceinline__ void decode_unit(int unit, const GemmArgs& p, bool fused,
-                                            TileCoord& tc, int& c0, int& nc) {
+                                            TileCoord& tc, int& c0, int& nc, int mc_rank = -1) {
   int tile;
-  decode_unit(unit, p, fused, tc, c0, nc, tile);
+  decode_unit(unit, p, fused, tc, c0, nc, tile, mc_rank);
 }
 
 __device__ __forceinline__ int ld_acquire_gpu(const int* ptr) {
@@ -185,12 +220,21 @@ __device__ __forceinline__ void store_staged(const GemmArgs& p, const double* st
   __syncwarp();
 }
 
-template <int W>
+// MC: launched as 2-CTA clusters; the two CTAs compute vertically adjacent
+// 128 x 256 tiles with the same B panel, each loading half of every B stage
+// and multicasting it to both (L2 -> SM operand traffic 64 KB instead of
+// 96 KB per 2 x 128 x 256 x 128 step).  A stage is refilled only after both
+// CTAs' MMAs released it (empty barriers count 2, commits multicast).
+template <int W, bool MC>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_i8_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
                    const GemmArgs p) {
   constexpr bool kFused = W >= 2;
   constexpr bool kFinal = W == 1;
+  static_assert(!MC || W == 0, "multicast is a split-mode variant");
+  const int mc_rank = MC ? static_cast<int>(cluster_ctarank()) : -1;
+  const int unit0 = MC ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+  const int ustep = MC ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -209,7 +253,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC ? 2 : 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -221,7 +265,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
   if (warp == 2) tmem_alloc(tmem_holder, kTmemCols);
   tc_fence_before();
-  __syncthreads();
+  if constexpr (MC)
+    cluster_sync();  // the peer's barriers exist before any multicast lands
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
@@ -229,12 +276,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // ---------------- TMA producer (warp-wide loop, one elected issuer) ----------------
     int stage = 0;
     uint32_t phase = 0;
-    for (int unit = blockIdx.x; unit < p.total_units; unit += gridDim.x) {
+    for (int unit = unit0; unit < p.total_units; unit += ustep) {
       TileCoord tc;
       int c0, nc;
-      decode_unit(unit, p, kFused, tc, c0, nc);
+      decode_unit(unit, p, kFused, tc, c0, nc, mc_rank);
       for (int c = c0; c < c0 + nc; ++c) {
-        const ChunkDesc cd = p.chunks[c];
+        const ChunkDesc cd = p.chunks[chunk_at(p, c)];
         for (int pr = 0; pr < cd.npairs; ++pr) {
           const int l = cd.l0 + pr;
           const int h = cd.d + 2 - l;
@@ -244,8 +291,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               mbar_expect_tx(&full[stage], kStageBytes);
               tma_load_3d(sA + stage * kABytes, &tma, &full[stage], kb * kBlockK,
                           tc.tm * kBlockM, l - 1);
-              tma_load_3d(sB + stage * kBBytes, &tmb, &full[stage], kb * kBlockK, tc.tn * kBN,
-                          h - 1);
+              if constexpr (MC)
+                tma_load_3d_mc(sB + stage * kBBytes + mc_rank * (kBBytes / 2), &tmb,
+                               &full[stage], kb * kBlockK, tc.tn * kBN + mc_rank * (kBN / 2),
+                               h - 1, 3);
+              else
+                tma_load_3d(sB + stage * kBBytes, &tmb, &full[stage], kb * kBlockK,
+                            tc.tn * kBN, h - 1);
             }
             __syncwarp();
             if (++stage == kStages) {
@@ -264,12 +316,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    for (int unit = blockIdx.x; unit < p.total_units; unit += gridDim.x) {
+    for (int unit = unit0; unit < p.total_units; unit += ustep) {
       TileCoord tc;
       int c0, nc;
-      decode_unit(unit, p, kFused, tc, c0, nc);
+      decode_unit(unit, p, kFused, tc, c0, nc, mc_rank);
       for (int c = c0; c < c0 + nc; ++c, ++it) {
-        const ChunkDesc cd = p.chunks[c];
+        const ChunkDesc cd = p.chunks[chunk_at(p, c)];
         const int acc = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], aphase ^ 1);
@@ -286,7 +338,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
             for (int kk = 0; kk < kBlockK / 32; ++kk)
               tc_mma_i8(tmem_d, ad + 2 * kk, bd + 2 * kk, idesc, (i | kk) != 0);
-            tc_commit(&empty[stage]);
+            if constexpr (MC)
+              tc_commit_mc(&empty[stage], 3);
+            else
+              tc_commit(&empty[stage]);
             if (i == total - 1) tc_commit(&tfull[acc]);
           }
           __syncwarp();
@@ -305,15 +360,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if constexpr (kFused)
       scratch = p.scratch + static_cast<size_t>(blockIdx.x) * W * kBN * kBlockM;
     int it = 0;
-    for (int unit = blockIdx.x; unit < p.total_units; unit += gridDim.x) {
+    for (int unit = unit0; unit < p.total_units; unit += ustep) {
       TileCoord tc;
       int c0, nc, tile;
-      decode_unit(unit, p, kFused, tc, c0, nc, tile);
+      decode_unit(unit, p, kFused, tc, c0, nc, tile, mc_rank);
       const int row0 = tc.tm * kBlockM + q * 32;
       const int row = row0 + lane;
       long qrow = 0;
       if constexpr (kFused || kFinal) qrow = row < p.m ? __ldg(p.qa + row) : 0;
-      for (int c = c0; c < c0 + nc; ++c, ++it) {
+      for (int cpos = c0; cpos < c0 + nc; ++cpos, ++it) {
+        const int c = kFused ? cpos : chunk_at(p, cpos);
         const int acc = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
         mbar_wait(&tfull[acc], aphase);
@@ -400,7 +456,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (MC)
+    cluster_sync();  // no CTA leaves while its peer may still multicast into it
+  else
+    __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, kTmemCols);
@@ -610,13 +669,44 @@ static cudaError_t launch_t(const CUtensorMap* tma, const CUtensorMap* tmb, cons
                             int grid, int smem, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(gemm_i8_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(gemm_i8_kernel<W, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  gemm_i8_kernel<W><<<grid, kGemmThreads, smem, st>>>(*tma, *tmb, args);
+  gemm_i8_kernel<W, false><<<grid, kGemmThreads, smem, st>>>(*tma, *tmb, args);
   return cudaGetLastError();
+}
+
+cudaError_t launch_gemm_i8_mc(const CUtensorMap* tma, const CUtensorMap* tmb_half,
+                              const GemmArgs& args, int num_sms, cudaStream_t st,
+                              int64_t* launches) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_i8_kernel<0, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSplit);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  int clusters = num_sms / 2;
+  if (args.total_units < clusters) clusters = args.total_units;
+  if (clusters < 1) return cudaSuccess;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * clusters);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = kSmemSplit;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_i8_kernel<0, true>, *tma, *tmb_half, args);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e == cudaSuccess) ++*launches;
+  return e;
 }
 
 cudaError_t launch_gemm_i8(const CUtensorMap* tma, const CUtensorMap* tmb, const GemmArgs& args,

@@ -258,6 +258,53 @@ ChunkPlan build_chunks(const ozgpu_plan& p, const ozgpu_mma_config& cfg, int64_t
   return cp;
 }
 
+// Bins of the split-mode GEMM: chunks packed (first-fit decreasing) into
+// runs with the same total pair count, so every unit of the pair GEMM has the
+// same length and the CTAs of a wave stay in step (they then stream the same
+// slice pair at the same time and share it through L2).  Tries bin sizes
+// from the largest chunk upward and keeps the first packing in which every
+// bin is full; returns false (no bins) if none is.  For the reduced schedule
+// the diagonals 1..L pair up as (1, L), (2, L-1), ... into bins of L + 1.
+bool build_bins(const std::vector<ChunkDesc>& chunks, std::vector<int>& order,
+                std::vector<int>& first) {
+  const int nc = static_cast<int>(chunks.size());
+  if (nc < 2) return false;
+  int total = 0, maxlen = 0;
+  for (const auto& c : chunks) {
+    total += c.npairs;
+    maxlen = std::max(maxlen, c.npairs);
+  }
+  std::vector<int> idx(nc);
+  for (int i = 0; i < nc; ++i) idx[i] = i;
+  std::stable_sort(idx.begin(), idx.end(),
+                   [&](int a, int b) { return chunks[a].npairs > chunks[b].npairs; });
+  for (int cap = maxlen; cap <= 2 * maxlen; ++cap) {
+    if (total % cap) continue;
+    std::vector<std::vector<int>> bins;
+    std::vector<int> fill;
+    for (int i : idx) {
+      size_t b = 0;
+      while (b < bins.size() && fill[b] + chunks[i].npairs > cap) ++b;
+      if (b == bins.size()) {
+        bins.emplace_back();
+        fill.push_back(0);
+      }
+      bins[b].push_back(i);
+      fill[b] += chunks[i].npairs;
+    }
+    if (static_cast<int>(bins.size()) * cap != total) continue;
+    order.clear();
+    first.clear();
+    for (auto& b : bins) {
+      first.push_back(static_cast<int>(order.size()));
+      order.insert(order.end(), b.begin(), b.end());
+    }
+    first.push_back(static_cast<int>(order.size()));
+    return true;
+  }
+  return false;
+}
+
 // Diagnostics exactly as the reference accumulates them (scheme.cpp:246-359).
 ozgpu_diag make_diag(const ozgpu_plan& p, const ozgpu_mma_config& cfg, int64_t m, int64_t n,
                      int64_t k, long long realized_psi) {
@@ -536,7 +583,33 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
         ctx->launches += launches;
         return nullptr;
       }
-      OZ_CUDA(launch_gemm_i8(&tma, &tmb, g, ctx->num_sms, st, &launches));
+      // Equal-length bins of chunks per unit (default when every CTA gets
+      // several units; OZGPU_BINS=0/1 overrides).
+      bool bins = tiles * g.nchunks >= 4 * static_cast<int64_t>(ctx->num_sms);
+      if (const char* env = std::getenv("OZGPU_BINS")) bins = std::string(env) == "1";
+      std::vector<int>& aux = ctx->host_aux;
+      std::vector<int> bfirst;
+      if (bins && build_bins(cp.chunks, aux, bfirst)) {
+        const size_t nb = bfirst.size() - 1;
+        aux.insert(aux.end(), bfirst.begin(), bfirst.end());
+        int* daux = static_cast<int*>(ctx->aux.get(sizeof(int) * aux.size()));
+        OZ_CUDA(cudaMemcpyAsync(daux, aux.data(), sizeof(int) * aux.size(),
+                                cudaMemcpyHostToDevice, st));
+        g.proc_order = daux;
+        g.bin_first = daux + g.nchunks;
+        g.total_units = static_cast<int>(tiles * static_cast<int64_t>(nb));
+      }
+      // 2-CTA clusters multicasting the shared B panel (OZGPU_MC=1)
+      bool mc = false;
+      if (const char* env = std::getenv("OZGPU_MC")) mc = std::string(env) == "1" && tiles_m >= 2;
+      if (mc) {
+        const int64_t super_tiles = static_cast<int64_t>((tiles_m + 1) / 2) * tiles_n;
+        g.total_units = static_cast<int>(g.total_units / tiles * super_tiles);
+        CUtensorMap tmb_half = make_slice_map(ctx, slB, kp, n, sb, 128);
+        OZ_CUDA(launch_gemm_i8_mc(&tma, &tmb_half, g, ctx->num_sms, st, &launches));
+      } else {
+        OZ_CUDA(launch_gemm_i8(&tma, &tmb, g, ctx->num_sms, st, &launches));
+      }
     }
     if (ctx->timing) OZ_CUDA(cudaEventRecord(ev[2], st));
 

@@ -45,6 +45,7 @@ struct GemmArgs {
   // the other chunks' planes diagonal by diagonal (diag_first) Horner-style,
   // rounds and stores C
   const int* proc_order;   // position -> chunk id (null = identity)
+  const int* bin_first;    // split mode: bin b = positions [bin_first[b], bin_first[b+1]) (null = 1 chunk per unit)
   int final_chunk;
   int* tile_counters;
   const int* diag_first;   // diagonals + 1 entries
@@ -98,6 +99,9 @@ cudaError_t launch_slice_cols(const double* b, int64_t ldb, int64_t k, int64_t n
                               cudaStream_t st, int64_t* launches);
 cudaError_t launch_gemm_i8(const CUtensorMap* tma, const CUtensorMap* tmb, const GemmArgs& args,
                            int num_sms, cudaStream_t st, int64_t* launches);
+cudaError_t launch_gemm_i8_mc(const CUtensorMap* tma, const CUtensorMap* tmb_half,
+                              const GemmArgs& args, int num_sms, cudaStream_t st,
+                              int64_t* launches);
 cudaError_t launch_gemm_i8_pair(const CUtensorMap* tma, const CUtensorMap* tmb,
                                 const GemmArgs& args, int num_sms, cudaStream_t st,
                                 int64_t* launches);

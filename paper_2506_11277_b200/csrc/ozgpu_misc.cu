@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "ozgpu_internal.h"
 #include "ozgpu_numeric.h"
@@ -260,6 +262,83 @@ __global__ void __launch_bounds__(256) combine_horner2_v4_kernel(const CombineAr
   }
 }
 
+// 128-bit Horner combine on (hi, lo) word pairs: per chunk (diagonal-major
+// order) V = (V << shift_c) + S_c with constant-cost funnel shifts (shift_c =
+// t times the diagonal step, < 64) and a carry-chained add, then round_hilo
+// (two exact conversions + one IEEE add on the common path).  About a third
+// of the instructions of the __int128 Horner kernels, so it streams the
+// chunk planes at HBM rate instead of being issue-bound.
+struct HiloProgram {
+  int shift[64];
+  int final_shift;
+};
+
+__device__ __forceinline__ void hilo_shift(uint64_t& hi, uint64_t& lo, int sh) {
+  // 0 <= sh < 64 (sh == 0: unchanged)
+  hi = sh ? (hi << sh) | (lo >> (64 - sh)) : hi;
+  lo = lo << sh;
+}
+__device__ __forceinline__ void hilo_add(uint64_t& hi, uint64_t& lo, int32_t s) {
+  const int64_t s64 = s;
+  asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;"
+      : "+l"(lo), "+l"(hi)
+      : "l"(static_cast<uint64_t>(s64)), "l"(static_cast<uint64_t>(s64 >> 63)));
+}
+
+__global__ void __launch_bounds__(256) combine_hilo_v4_kernel(const CombineArgs p,
+                                                              const HiloProgram hp) {
+  const int64_t groups_per_row = p.n / 4;
+  const int64_t total = static_cast<int64_t>(p.m) * groups_per_row;
+  const bool vec_c = (p.ldc & 1) == 0 && (reinterpret_cast<uintptr_t>(p.c) & 15) == 0;
+  const int64_t stride4 = p.plane_stride / 4;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = idx / groups_per_row, j = (idx - i * groups_per_row) * 4;
+    const int4* src = reinterpret_cast<const int4*>(p.planes + i * p.ldp + j);
+    uint64_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
+    for (int cb = 0; cb < p.nchunks; cb += 16) {
+      int4 s[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (cb + u < p.nchunks) s[u] = __ldcs(src + (cb + u) * stride4);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        if (cb + u < p.nchunks) {
+          const int sh = hp.shift[cb + u];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) hilo_shift(hi[e], lo[e], sh);
+          hilo_add(hi[0], lo[0], s[u].x);
+          hilo_add(hi[1], lo[1], s[u].y);
+          hilo_add(hi[2], lo[2], s[u].z);
+          hilo_add(hi[3], lo[3], s[u].w);
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) hilo_shift(hi[e], lo[e], hp.final_shift);
+    const long qi = static_cast<long>(__ldg(p.qa + i)) + p.w_last;
+    const int4 qb = __ldg(reinterpret_cast<const int4*>(p.qb + j));
+    double r[4];
+    r[0] = round_hilo(hi[0], lo[0], qi + qb.x);
+    r[1] = round_hilo(hi[1], lo[1], qi + qb.y);
+    r[2] = round_hilo(hi[2], lo[2], qi + qb.z);
+    r[3] = round_hilo(hi[3], lo[3], qi + qb.w);
+    if (p.axpby) {  // two roundings, no FMA contraction (scheme.cpp:369-370)
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        r[e] = __dadd_rn(__dmul_rn(p.alpha, r[e]), __dmul_rn(p.beta, p.cin[i * p.ldcin + j + e]));
+    }
+    double* dst = p.c + i * p.ldc + j;
+    if (vec_c) {
+      __stcs(reinterpret_cast<double2*>(dst), make_double2(r[0], r[1]));
+      __stcs(reinterpret_cast<double2*>(dst) + 1, make_double2(r[2], r[3]));
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) dst[e] = r[e];
+    }
+  }
+}
+
 // Sequential FP64 accumulation in the reference order (d ascending, l
 // ascending) with the TwoSum inexact counter (scheme.cpp:173-215).
 __global__ void __launch_bounds__(256) combine_sequential_kernel(const CombineArgs p) {
@@ -494,6 +573,20 @@ cudaError_t launch_combine_exact(const CombineArgs& args, int words, const Chunk
       CombineArgs a2 = args;
       a2.hgroup = std::max(1, 1 + (62 - (31 + lg)) / std::max(1, args.width));
       const int grid = grid_for(total / 4, 256, 148 * 8);
+      const char* hv = std::getenv("OZGPU_COMBINE");
+      if (args.nchunks <= 64 && args.width < 64 && !(hv && std::string(hv) == "horner")) {
+        HiloProgram hp{};
+        for (int c = 1; c < args.nchunks; ++c)
+          hp.shift[c] = (host_chunks[c].d - host_chunks[c - 1].d) * args.width;
+        hp.final_shift = (args.diagonals - 1 - host_chunks[args.nchunks - 1].d) * args.width;
+        bool ok = hp.final_shift < 64;
+        for (int c = 1; c < args.nchunks; ++c) ok &= hp.shift[c] < 64;
+        if (ok) {
+          combine_hilo_v4_kernel<<<grid, 256, 0, st>>>(args, hp);
+          ++*launches;
+          return cudaGetLastError();
+        }
+      }
       if (args.nchunks <= 64) {
         HornerProgram hp{};
         int run_len = 0;

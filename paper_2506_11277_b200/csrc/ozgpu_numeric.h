@@ -274,4 +274,39 @@ OZ_HD double round_i128(unsigned __int128 v, long e) {
   return neg ? -r : r;
 }
 
+// 2^x as a double, x in [-1022, 1023] (normal range only).
+OZ_HD double pow2_normal(long x) { return bits_dbl(static_cast<uint64_t>(x + 1023) << 52); }
+
+// RN(v * 2^e) for the signed 128-bit value v = hi * 2^64 + lo (lo unsigned)
+// -- the same result as round_i128 (and so ExactValue::to_double,
+// oracle.cpp:157-180) but with two exact conversions and one IEEE add on the
+// common path:
+//   v = H + L with H = hi * 2^64 (exact in a double while |hi| < 2^53) and
+//   L = lo.  Rounding L to odd at granularity 2^11, L' = ((lo >> 11) | sticky)
+//   * 2^11, is exact in a double (53 bits) and commutes with adding H (a
+//   multiple of 2^12).  When |v| >= 2^65 (hi >= 2 or hi <= -3) the result's
+//   ulp is >= 2^13 = 4 * 2^11, so RN(H + L') == RN(v) (round-to-odd with two
+//   extra bits, Boldo-Melquiond), and the IEEE add of the two exact scaled
+//   terms rounds once.  The scale 2^e is applied to both terms exactly while
+//   -1033 <= e <= 900 (no subnormal or overflowing intermediate, result
+//   normal).  Everything else takes round_i128.
+OZ_HD double round_hilo(uint64_t hi, uint64_t lo, long e) {
+  const int64_t h = static_cast<int64_t>(hi);
+  const bool big = (h >= 2 || h <= -3) && h < (int64_t{1} << 53) && h > -(int64_t{1} << 53);
+  if (big && e >= -1033 && e <= 900) {
+#ifdef __CUDA_ARCH__
+    const double hf = __dmul_rn(__ll2double_rn(h), pow2_normal(64 + e));
+    const double lf = __dmul_rn(__ull2double_rn((lo >> 11) | ((lo & 0x7FF) != 0)),
+                                pow2_normal(11 + e));
+    return __dadd_rn(hf, lf);
+#else
+    const double hf = static_cast<double>(h) * pow2_normal(64 + e);
+    const double lf = static_cast<double>((lo >> 11) | ((lo & 0x7FF) != 0)) * pow2_normal(11 + e);
+    return hf + lf;
+#endif
+  }
+  const unsigned __int128 v = (static_cast<unsigned __int128>(hi) << 64) | lo;
+  return round_i128(v, e);
+}
+
 }  // namespace ozgpu

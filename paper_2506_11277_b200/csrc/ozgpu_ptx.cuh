@@ -196,4 +196,26 @@ __host__ __device__ constexpr uint32_t idesc_i8() {
          (static_cast<uint32_t>(M >> 4) << 24);
 }
 
+// ---- 1-CTA MMA with TMA multicast inside a 2-CTA cluster -----------------
+
+// TMA load multicast to the CTAs in `mask`: the box lands at the same smem
+// offset in each and completes tx bytes on the same mbarrier offset in each.
+__device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                               int c0, int c1, int c2, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_addr(bar)), "r"(c0), "r"(c1), "r"(c2),
+      "h"(mask)
+      : "memory");
+}
+// commit this CTA's MMAs to the same mbarrier offset in the CTAs of `mask`
+__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_addr(bar)),
+      "h"(mask)
+      : "memory");
+}
+
 }  // namespace ozgpu

@@ -42,3 +42,5 @@ extern "C" double nt_round_i128(uint64_t lo, uint64_t hi, long e) {
   unsigned __int128 v = (static_cast<unsigned __int128>(hi) << 64) | lo;
   return round_i128(v, e);
 }
+
+extern "C" double nt_round_hilo(uint64_t lo, uint64_t hi, long e) { return round_hilo(hi, lo, e); }

@@ -232,13 +232,28 @@ def test_native_kernels_launched(oz):
     assert oz.kernel_launches() - before >= 4
 
 
-@pytest.mark.parametrize("mode,pair", [("default", "0"), ("final", "0"), ("fused", "0"), ("split", "1")])
-def test_gemm_variants_match_reference(oz, ref, mode, pair, monkeypatch):
+GEMM_VARIANTS = {
+    "default": {},
+    "final": {"OZGPU_EPILOGUE": "final"},
+    "fused": {"OZGPU_EPILOGUE": "fused"},
+    "cta_pair": {"OZGPU_EPILOGUE": "split", "OZGPU_CTA_PAIR": "1"},
+    "bins": {"OZGPU_BINS": "1"},
+    "no_bins": {"OZGPU_BINS": "0"},
+    "multicast": {"OZGPU_MC": "1"},
+    "multicast_bins": {"OZGPU_MC": "1", "OZGPU_BINS": "1"},
+    "horner_combine": {"OZGPU_COMBINE": "horner"},
+}
+
+
+@pytest.mark.parametrize("variant", sorted(GEMM_VARIANTS))
+def test_gemm_variants_match_reference(oz, ref, variant, monkeypatch):
     """Every GEMM variant -- fused exact-integer epilogue, split planes +
-    combine on the CTA-pair (cta_group::2) kernel and on the 1-CTA kernel --
-    is bit-exact, incl. ragged tiles and 3-word exact values."""
-    monkeypatch.setenv("OZGPU_EPILOGUE", mode)
-    monkeypatch.setenv("OZGPU_CTA_PAIR", pair)
+    combine on the CTA-pair (cta_group::2) kernel and on the 1-CTA kernel,
+    equal-length chunk bins, B-panel multicast in 2-CTA clusters, both exact
+    combine kernels -- is bit-exact, incl. ragged tiles and 3-word exact
+    values."""
+    for key, val in GEMM_VARIANTS[variant].items():
+        monkeypatch.setenv(key, val)
     rng = np.random.default_rng(77)
     cfg = oz.MmaConfig.int8_int32()
     for (m, k, n) in [(128, 256, 256), (300, 500, 700), (520, 128, 260)]:

@@ -141,3 +141,44 @@ def test_round_i128_matches_bigints(nt):
         got = nt.nt_round_i128(u & ((1 << 64) - 1), u >> 64, e)
         want = _exact_round(v, e)
         assert got == want or (math.isinf(got) and math.isinf(want)), (v, e, got, want)
+
+
+def test_round_hilo_fast_path_matches_exact(nt):
+    """round_hilo (two exact conversions + one IEEE add, the combine's
+    common path) equals ExactValue::to_double on random, tie-heavy and
+    boundary 128-bit values (|hi| around 2..4, sticky-only low words,
+    exact midpoints)."""
+    nt.nt_round_hilo.restype = ctypes.c_double
+    nt.nt_round_hilo.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_long]
+    rng = np.random.default_rng(7)
+    cases = []
+    for trial in range(40000):
+        kind = trial % 5
+        if kind == 0:
+            bits = int(rng.integers(1, 120))
+            v = int(rng.integers(0, 2**62)) << max(0, bits - 62)
+        elif kind == 1:  # near the fast-path boundary |v| ~ 2^64 .. 2^67
+            v = int(rng.integers(2**31, 2**35)) << 32 | int(rng.integers(0, 2**32))
+        elif kind == 2:  # exact ties at 53 bits: top 54 bits then zeros (+ optional sticky)
+            nb = int(rng.integers(66, 118))
+            top = int(rng.integers(2**53, 2**54)) | 1
+            v = top << (nb - 54)
+            if trial % 10 == 2:
+                v += 1
+        elif kind == 3:  # long carry chains in the low word
+            nb = int(rng.integers(66, 118))
+            v = (int(rng.integers(1, 2**20)) << (nb - 20)) - int(rng.integers(0, 2**12))
+        else:  # sticky bits only below bit 11 of the low word
+            v = (int(rng.integers(2**40, 2**53)) << 64) + int(rng.integers(0, 2**11))
+        if trial % 2:
+            v = -v
+        e = int(rng.integers(-1100, 950)) if trial % 7 == 0 else int(rng.integers(-300, 100))
+        cases.append((v, e))
+    for v, e in cases + [(2**65, -100), (-(2**65), -100), (3 * 2**64, 5), (-(3 * 2**64) + 1, 5),
+                         (2**64 + 1, 0), (-(2**64) - 1, 0), (2**116 + 2**63, -1033),
+                         (2**116 - 1, 900)]:
+        u = v % (1 << 128)
+        got = nt.nt_round_hilo(u & ((1 << 64) - 1), u >> 64, e)
+        want = _exact_round(v, e)
+        assert got == want or (math.isinf(got) and math.isinf(want)), (v, e, got, want)
+        assert math.copysign(1, got) == math.copysign(1, want) or want == 0, (v, e)
