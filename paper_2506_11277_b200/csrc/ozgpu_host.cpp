@@ -114,7 +114,7 @@ struct ozgpu_ctx {
   ozgpu::DevBuf aux, counters;
   // row-blocked H2D / compute / D2H pipeline of ozgpu_dgemm
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
-  cudaEvent_t pipe_events[10] = {};
+  std::vector<cudaEvent_t> pipe_events;
   // stage timing (ozgpu_set_stage_timing)
   bool timing = false;
   std::vector<std::array<cudaEvent_t, 4>> pending_events;
@@ -166,11 +166,12 @@ CUtensorMapL2promotion l2_promotion() {
 // 3-D int8 tensor map over slices [count][rows][kp], box {128, box_rows, 1},
 // 128-byte swizzle (matches the UMMA SW128 K-major descriptor).
 CUtensorMap make_slice_map(ozgpu_ctx* ctx, const void* base, int64_t kp, int64_t rows,
-                           int count, int box_rows) {
+                           int count, int box_rows, int64_t plane = 0) {
   CUtensorMap m;
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(kp), static_cast<cuuint64_t>(rows),
                         static_cast<cuuint64_t>(count)};
-  cuuint64_t strides[2] = {static_cast<cuuint64_t>(kp), static_cast<cuuint64_t>(kp * rows)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(kp),
+                           static_cast<cuuint64_t>(plane ? plane : kp * rows)};
   cuuint32_t box[3] = {static_cast<cuuint32_t>(kBlockK), static_cast<cuuint32_t>(box_rows), 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = ctx->encode(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims,
@@ -392,15 +393,25 @@ int exact_words(int diagonals, int width, size_t nchunks) {
   throw std::invalid_argument("multiply: exact accumulator wider than 1024 bits");
 }
 
+// Operands already sliced by the caller (the blocked pipeline of
+// host_multiply): a row range of the [count][rows][kp] slice buffers, with
+// the full buffers' plane stride, and the matching scales.
+struct Presliced {
+  const int8_t* a;
+  int64_t plane_a;
+  const int* qa;
+  const int8_t* b;
+  int64_t plane_b;
+  const int* qb;
+};
+
 // The device-resident core of multiply(): everything is enqueued on `st`.
 // Returns the realized psi device pointer (sequential strategies) or null.
 int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* da, int64_t lda,
                   const double* db, int64_t ldb, double* dc, int64_t ldc,
                   const ozgpu_mma_config& cfg, const ozgpu_plan& p, cudaStream_t st,
                   int* dev_status, bool axpby, double alpha, double beta, const double* dcin,
-                  int64_t ldcin, bool reuse_b = false) {
-  // reuse_b: B's slices / scales / status from the previous call on this
-  // stream are still valid (row-blocked pipeline of host_multiply)
+                  int64_t ldcin, const Presliced* pre = nullptr) {
   int64_t launches = 0;
   std::array<cudaEvent_t, 4> ev{};
   if (ctx->timing) {
@@ -417,18 +428,35 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
   const int64_t kp = round_up(k, kKPad);
   ChunkPlan cp = build_chunks(p, cfg, k);
 
-  int8_t* slA = static_cast<int8_t*>(ctx->slices_a.get(static_cast<size_t>(sa) * m * kp + 1));
-  int8_t* slB = static_cast<int8_t*>(ctx->slices_b.get(static_cast<size_t>(sb) * n * kp + 1));
-  int* qa = static_cast<int*>(ctx->qa.get(sizeof(int) * (m + 1)));
-  int* qb = static_cast<int*>(ctx->qb.get(sizeof(int) * (n + 1)));
-  auto* colmax = static_cast<unsigned long long*>(ctx->colmax.get(8 * (n + 1)));
-  int* status = dev_status ? dev_status : static_cast<int*>(ctx->status.get(sizeof(int)));
-  if (!reuse_b) OZ_CUDA(cudaMemsetAsync(status, 0, sizeof(int), st));
-
-  OZ_CUDA(launch_slice_rows(da, lda, m, k, kp, t, sa, p.mode, slA, 0, qa, status, st, &launches));
-  if (!reuse_b)
-    OZ_CUDA(launch_slice_cols(db, ldb, k, n, kp, t, sb, p.mode, slB, 0, qb, colmax, status, st,
+  const int8_t* slA;
+  const int8_t* slB;
+  const int* qa;
+  const int* qb;
+  int64_t plane_a = m * kp, plane_b = n * kp;
+  if (pre) {
+    slA = pre->a;
+    slB = pre->b;
+    qa = pre->qa;
+    qb = pre->qb;
+    plane_a = pre->plane_a;
+    plane_b = pre->plane_b;
+  } else {
+    int8_t* wa = static_cast<int8_t*>(ctx->slices_a.get(static_cast<size_t>(sa) * m * kp + 1));
+    int8_t* wb = static_cast<int8_t*>(ctx->slices_b.get(static_cast<size_t>(sb) * n * kp + 1));
+    int* wqa = static_cast<int*>(ctx->qa.get(sizeof(int) * (m + 1)));
+    int* wqb = static_cast<int*>(ctx->qb.get(sizeof(int) * (n + 1)));
+    auto* colmax = static_cast<unsigned long long*>(ctx->colmax.get(8 * (n + 1)));
+    int* status = dev_status ? dev_status : static_cast<int*>(ctx->status.get(sizeof(int)));
+    OZ_CUDA(cudaMemsetAsync(status, 0, sizeof(int), st));
+    OZ_CUDA(launch_slice_rows(da, lda, m, k, kp, t, sa, p.mode, wa, 0, wqa, status, st,
                               &launches));
+    OZ_CUDA(launch_slice_cols(db, ldb, k, n, kp, t, sb, p.mode, wb, 0, wqb, colmax, status, st,
+                              &launches));
+    slA = wa;
+    slB = wb;
+    qa = wqa;
+    qb = wqb;
+  }
   if (ctx->timing) OZ_CUDA(cudaEventRecord(ev[1], st));
 
   int* psi_dev = nullptr;
@@ -468,8 +496,8 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
                             cudaMemcpyHostToDevice, st));
     ctx->host_chunks = cp.chunks;
 
-    CUtensorMap tma = make_slice_map(ctx, slA, kp, m, sa, kBlockM);
-    CUtensorMap tmb = make_slice_map(ctx, slB, kp, n, sb, 256);
+    CUtensorMap tma = make_slice_map(ctx, slA, kp, m, sa, kBlockM, plane_a);
+    CUtensorMap tmb = make_slice_map(ctx, slB, kp, n, sb, 256, plane_b);
     GemmArgs g{};
     g.chunks = dchunks;
     g.nchunks = static_cast<int>(cp.chunks.size());
@@ -524,7 +552,7 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
     if (pair) {
       g.tiles_m = static_cast<int>((m + 255) / 256);
       g.total_units = pair_tiles * g.nchunks;
-      CUtensorMap tmb2 = make_slice_map(ctx, slB, kp, n, sb, 128);
+      CUtensorMap tmb2 = make_slice_map(ctx, slB, kp, n, sb, 128, plane_b);
       OZ_CUDA(launch_gemm_i8_pair(&tma, &tmb2, g, ctx->num_sms, st, &launches));
     } else {
       g.total_units = static_cast<int>(tiles * g.nchunks);
@@ -599,13 +627,17 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
         g.bin_first = daux + g.nchunks;
         g.total_units = static_cast<int>(tiles * static_cast<int64_t>(nb));
       }
-      // 2-CTA clusters multicasting the shared B panel (OZGPU_MC=1)
-      bool mc = false;
+      // 2-CTA clusters multicasting the shared B panel (default; OZGPU_MC=0
+      // selects the plain 1-CTA launch): measured on B200 at 8192^3 (12,12)
+      // under the power cap, 30.3 vs 34.4 ms per pair-GEMM launch (8
+      // interleaved rounds) -- a third less L2->SM operand traffic lets the
+      // SM clock run ~5% higher at the same board power.
+      bool mc = tiles_m >= 2;
       if (const char* env = std::getenv("OZGPU_MC")) mc = std::string(env) == "1" && tiles_m >= 2;
       if (mc) {
         const int64_t super_tiles = static_cast<int64_t>((tiles_m + 1) / 2) * tiles_n;
         g.total_units = static_cast<int>(g.total_units / tiles * super_tiles);
-        CUtensorMap tmb_half = make_slice_map(ctx, slB, kp, n, sb, 128);
+        CUtensorMap tmb_half = make_slice_map(ctx, slB, kp, n, sb, 128, plane_b);
         OZ_CUDA(launch_gemm_i8_mc(&tma, &tmb_half, g, ctx->num_sms, st, &launches));
       } else {
         OZ_CUDA(launch_gemm_i8(&tma, &tmb, g, ctx->num_sms, st, &launches));
@@ -700,47 +732,146 @@ void host_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double
   double* db = static_cast<double*>(ctx->in_b.get(sizeof(double) * k * n + 8));
   const std::string perr = plan_error(p);
   const bool failing = k < 1 || v.capacity_error || v.precision_error || !perr.empty();
-  // Row-blocked pipeline for large products: B goes over PCIe first and is
-  // sliced once; A arrives in row blocks on a copy stream, each block is
-  // sliced + multiplied on the compute stream as soon as it lands, and its C
-  // rows go back on a third stream while the next block computes.
+  // Blocked H2D / compute / D2H pipeline for large products.  A arrives in
+  // row blocks; the first row block is multiplied against B column panel by
+  // column panel as the panels land (so the tensor cores start after one A
+  // block + one B panel instead of all of B), the other row blocks against
+  // the whole of B, the last one in column halves so that only a small C
+  // block is left to copy back after the final GEMM.  Every block's C goes
+  // back on the D2H stream as soon as its combine is done.  Blocking is
+  // exact: scales are per row of A and per column of B.
   const int64_t bytes = 8 * (m * k + k * n + m * n);
-  const int nblk = (!failing && !axpby && p.strategy == 2 && m >= 2048 && bytes >= (64 << 20))
-                       ? 4 : 1;
-  if (nblk > 1) {
+  auto env_int = [](const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v ? std::atoi(v) : dflt;
+  };
+  const bool pipeline = !failing && !axpby && p.strategy == 2 && m >= 2048 && n >= 1024 &&
+                        bytes >= (64 << 20) && env_int("OZGPU_PIPE", 1) == 1;
+  if (pipeline) {
+    // measured on B200 (PCIe ~52 GB/s each way) at 8192^3 (12,12): 4 row
+    // blocks with the first one in 4 column panels, the last in 2 halves
+    const int nblk = std::max(1, env_int("OZGPU_PIPE_ROWS", 4));
+    const int npan = std::max(1, env_int("OZGPU_PIPE_PANELS", 4));
+    const int nlast = std::max(1, env_int("OZGPU_PIPE_LAST", 2));
     if (!ctx->h2d_stream) {
       OZ_CUDA(cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
       OZ_CUDA(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
-      for (auto& e : ctx->pipe_events) OZ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
-    cudaEvent_t* ev = ctx->pipe_events;  // [0] B in, [1..4] A blocks in, [5..8] C blocks out
+    const int t = p.width;
+    const int64_t kp = round_up(k, kKPad);
     double* dc = static_cast<double*>(ctx->io_c.get(sizeof(double) * m * n + 8));
-    OZ_CUDA(cudaEventRecord(ev[9], st));  // order after earlier work on the compute stream
-    OZ_CUDA(cudaStreamWaitEvent(ctx->h2d_stream, ev[9], 0));
-    h2d(db, b, k, n, ldb, ctx->h2d_stream);
-    OZ_CUDA(cudaEventRecord(ev[0], ctx->h2d_stream));
-    const int64_t rows = round_up((m + nblk - 1) / nblk, 128);
-    for (int r = 0; r < nblk; ++r) {
-      const int64_t r0 = std::min(m, r * rows), r1 = std::min(m, r0 + rows);
-      h2d(da + r0 * k, a + r0 * lda, r1 - r0, k, lda, ctx->h2d_stream);
-      OZ_CUDA(cudaEventRecord(ev[1 + r], ctx->h2d_stream));
+    int8_t* slA =
+        static_cast<int8_t*>(ctx->slices_a.get(static_cast<size_t>(p.slices_a) * m * kp + 1));
+    int8_t* slB =
+        static_cast<int8_t*>(ctx->slices_b.get(static_cast<size_t>(p.slices_b) * n * kp + 1));
+    int* qa = static_cast<int*>(ctx->qa.get(sizeof(int) * (m + 1)));
+    int* qb = static_cast<int*>(ctx->qb.get(sizeof(int) * (n + 1)));
+    auto* colmax = static_cast<unsigned long long*>(ctx->colmax.get(8 * (n + 1)));
+    int* status = static_cast<int*>(ctx->status.get(sizeof(int)));
+    // row blocks (multiples of 256 rows) and column panels (multiples of 256)
+    std::vector<int64_t> rb{0}, cb{0};
+    const int64_t rows = round_up((m + nblk - 1) / nblk, 256);
+    while (rb.back() < m) rb.push_back(std::min(m, rb.back() + rows));
+    auto split_cols = [&](int parts) {
+      std::vector<int64_t> e{0};
+      const int64_t w = round_up((n + parts - 1) / parts, 256);
+      while (e.back() < n) e.push_back(std::min(n, e.back() + w));
+      return e;
+    };
+    cb = split_cols(npan);
+    const std::vector<int64_t> cl = split_cols(nlast);
+    const size_t nr = rb.size() - 1, nc = cb.size() - 1;
+    const size_t nev = 1 + nr + nc + nr * std::max(nc, cl.size()) + 4;
+    while (ctx->pipe_events.size() < nev) {
+      cudaEvent_t e;
+      OZ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ctx->pipe_events.push_back(e);
     }
-    OZ_CUDA(cudaStreamWaitEvent(st, ev[0], 0));
-    for (int r = 0; r < nblk; ++r) {
-      const int64_t r0 = std::min(m, r * rows), r1 = std::min(m, r0 + rows);
-      OZ_CUDA(cudaStreamWaitEvent(st, ev[1 + r], 0));
-      if (r1 > r0)
-        run_multiply(ctx, r1 - r0, n, k, da + r0 * k, k, db, n, dc + r0 * n, n, cfg, p, st,
-                     nullptr, false, 1.0, 0.0, nullptr, 0, /*reuse_b=*/r > 0);
-      OZ_CUDA(cudaEventRecord(ev[5 + r], st));
-      OZ_CUDA(cudaStreamWaitEvent(ctx->d2h_stream, ev[5 + r], 0));
-      d2h(c + r0 * ldc, ldc, dc + r0 * n, r1 - r0, n, ctx->d2h_stream);
+    size_t evi = 0;
+    auto next_event = [&]() { return ctx->pipe_events[evi++]; };
+    // OZGPU_PIPE_TRACE=1: timing events on every step, printed to stderr
+    const bool trace = env_int("OZGPU_PIPE_TRACE", 0) == 1;
+    std::vector<std::pair<std::string, cudaEvent_t>> marks;
+    auto mark = [&](const std::string& what, cudaStream_t s) {
+      if (!trace) return;
+      cudaEvent_t e;
+      OZ_CUDA(cudaEventCreate(&e));
+      OZ_CUDA(cudaEventRecord(e, s));
+      marks.emplace_back(what, e);
+    };
+    // inputs: A block 0, then the B panels, then the other A blocks
+    cudaEvent_t start = next_event();
+    OZ_CUDA(cudaMemsetAsync(status, 0, sizeof(int), st));
+    OZ_CUDA(cudaEventRecord(start, st));  // after earlier work on the compute stream
+    OZ_CUDA(cudaStreamWaitEvent(ctx->h2d_stream, start, 0));
+    mark("start", ctx->h2d_stream);
+    std::vector<cudaEvent_t> a_in(nr), b_in(nc);
+    auto copy_a = [&](size_t i) {
+      h2d(da + rb[i] * k, a + rb[i] * lda, rb[i + 1] - rb[i], k, lda, ctx->h2d_stream);
+      a_in[i] = next_event();
+      OZ_CUDA(cudaEventRecord(a_in[i], ctx->h2d_stream));
+      mark("h2d A" + std::to_string(i), ctx->h2d_stream);
+    };
+    copy_a(0);
+    for (size_t j = 0; j < nc; ++j) {  // panel j: k x nj, dense at db + k * c0
+      h2d(db + k * cb[j], b + cb[j], k, cb[j + 1] - cb[j], ldb, ctx->h2d_stream);
+      b_in[j] = next_event();
+      OZ_CUDA(cudaEventRecord(b_in[j], ctx->h2d_stream));
+      mark("h2d B" + std::to_string(j), ctx->h2d_stream);
     }
+    for (size_t i = 1; i < nr; ++i) copy_a(i);
+    int64_t launches = 0;
+    auto slice_a = [&](size_t i) {
+      OZ_CUDA(cudaStreamWaitEvent(st, a_in[i], 0));
+      OZ_CUDA(launch_slice_rows(da + rb[i] * k, k, rb[i + 1] - rb[i], k, kp, t, p.slices_a, p.mode,
+                                slA + rb[i] * kp, 0, qa + rb[i], status, st, &launches, m * kp));
+      mark("slice A" + std::to_string(i), st);
+    };
+    auto block = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1) {
+      Presliced pre{slA + r0 * kp, m * kp, qa + r0, slB + c0 * kp, n * kp, qb + c0};
+      run_multiply(ctx, r1 - r0, c1 - c0, k, nullptr, 0, nullptr, 0, dc + r0 * n + c0, n, cfg, p,
+                   st, nullptr, false, 1.0, 0.0, nullptr, 0, &pre);
+      cudaEvent_t done = next_event();
+      OZ_CUDA(cudaEventRecord(done, st));
+      const std::string tag = "C[" + std::to_string(r0) + ":" + std::to_string(r1) + "," +
+                              std::to_string(c0) + ":" + std::to_string(c1) + "]";
+      mark("gemm " + tag, st);
+      OZ_CUDA(cudaStreamWaitEvent(ctx->d2h_stream, done, 0));
+      OZ_CUDA(cudaMemcpy2DAsync(c + r0 * ldc + c0, ldc * sizeof(double), dc + r0 * n + c0,
+                                n * sizeof(double), (c1 - c0) * sizeof(double), r1 - r0,
+                                cudaMemcpyDeviceToHost, ctx->d2h_stream));
+      mark("d2h " + tag, ctx->d2h_stream);
+    };
+    slice_a(0);
+    for (size_t j = 0; j < nc; ++j) {
+      const int64_t nj = cb[j + 1] - cb[j];
+      OZ_CUDA(cudaStreamWaitEvent(st, b_in[j], 0));
+      OZ_CUDA(launch_slice_cols(db + k * cb[j], nj, k, nj, kp, t, p.slices_b, p.mode,
+                                slB + cb[j] * kp, 0, qb + cb[j], colmax + cb[j], status, st,
+                                &launches, n * kp));
+      block(rb[0], rb[1], cb[j], cb[j + 1]);
+    }
+    for (size_t i = 1; i < nr; ++i) {
+      slice_a(i);
+      if (i + 1 == nr && nr > 1) {
+        for (size_t j = 0; j + 1 < cl.size(); ++j) block(rb[i], rb[i + 1], cl[j], cl[j + 1]);
+      } else {
+        block(rb[i], rb[i + 1], 0, n);
+      }
+    }
+    ctx->launches += launches;
     int hs = 0;
-    OZ_CUDA(cudaMemcpyAsync(&hs, ctx->status.p, sizeof(int), cudaMemcpyDeviceToHost,
-                            ctx->d2h_stream));
+    OZ_CUDA(cudaMemcpyAsync(&hs, status, sizeof(int), cudaMemcpyDeviceToHost, ctx->d2h_stream));
     OZ_CUDA(cudaStreamSynchronize(ctx->d2h_stream));
     OZ_CUDA(cudaStreamSynchronize(st));
+    if (trace) {
+      for (auto& mk : marks) {
+        float ms = 0.f;
+        OZ_CUDA(cudaEventElapsedTime(&ms, marks[0].second, mk.second));
+        std::fprintf(stderr, "[ozgpu pipe] %8.3f ms  %s\n", ms, mk.first.c_str());
+      }
+      for (auto& mk : marks) cudaEventDestroy(mk.second);
+    }
     if (hs) throw std::invalid_argument("multiply: inputs must be finite with no negative zeros");
     if (diag) *diag = make_diag(p, cfg, m, n, k, 0);
     return;
@@ -884,8 +1015,8 @@ int ozgpu_destroy(ozgpu_ctx* ctx) {
       cudaStreamSynchronize(ctx->d2h_stream);
       cudaStreamDestroy(ctx->h2d_stream);
       cudaStreamDestroy(ctx->d2h_stream);
-      for (cudaEvent_t e : ctx->pipe_events) cudaEventDestroy(e);
     }
+    for (cudaEvent_t e : ctx->pipe_events) cudaEventDestroy(e);
     for (auto& ev : ctx->pending_events)
       for (cudaEvent_t e : ev) cudaEventDestroy(e);
     for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);

@@ -92,11 +92,12 @@ struct CombineArgs {
 // Launchers (return cudaError_t; 0 == success).  `launches` counts kernels.
 cudaError_t launch_slice_rows(const double* a, int64_t lda, int64_t m, int64_t k, int64_t kp,
                               int width, int count, int mode, void* out, int out_is_i64,
-                              int* scales, int* status, cudaStream_t st, int64_t* launches);
+                              int* scales, int* status, cudaStream_t st, int64_t* launches,
+                              int64_t plane = 0);
 cudaError_t launch_slice_cols(const double* b, int64_t ldb, int64_t k, int64_t n, int64_t kp,
                               int width, int count, int mode, void* out, int out_is_i64,
                               int* scales, unsigned long long* colmax, int* status,
-                              cudaStream_t st, int64_t* launches);
+                              cudaStream_t st, int64_t* launches, int64_t plane = 0);
 cudaError_t launch_gemm_i8(const CUtensorMap* tma, const CUtensorMap* tmb, const GemmArgs& args,
                            int num_sms, cudaStream_t st, int64_t* launches);
 cudaError_t launch_gemm_i8_mc(const CUtensorMap* tma, const CUtensorMap* tmb_half,

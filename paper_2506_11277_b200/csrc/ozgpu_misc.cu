@@ -285,8 +285,8 @@ __device__ __forceinline__ void hilo_add(uint64_t& hi, uint64_t& lo, int32_t s) 
       : "l"(static_cast<uint64_t>(s64)), "l"(static_cast<uint64_t>(s64 >> 63)));
 }
 
-__global__ void __launch_bounds__(256) combine_hilo_v4_kernel(const CombineArgs p,
-                                                              const HiloProgram hp) {
+__global__ void __launch_bounds__(256, 3) combine_hilo_v4_kernel(const CombineArgs p,
+                                                                 const HiloProgram hp) {
   const int64_t groups_per_row = p.n / 4;
   const int64_t total = static_cast<int64_t>(p.m) * groups_per_row;
   const bool vec_c = (p.ldc & 1) == 0 && (reinterpret_cast<uintptr_t>(p.c) & 15) == 0;
@@ -296,17 +296,19 @@ __global__ void __launch_bounds__(256) combine_hilo_v4_kernel(const CombineArgs 
     const int64_t i = idx / groups_per_row, j = (idx - i * groups_per_row) * 4;
     const int4* src = reinterpret_cast<const int4*>(p.planes + i * p.ldp + j);
     uint64_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
-    for (int cb = 0; cb < p.nchunks; cb += 16) {
-      int4 s[16];
+    for (int cb = 0; cb < p.nchunks; cb += 8) {
+      int4 s[8];
 #pragma unroll
-      for (int u = 0; u < 16; ++u)
+      for (int u = 0; u < 8; ++u)
         if (cb + u < p.nchunks) s[u] = __ldcs(src + (cb + u) * stride4);
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
+      for (int u = 0; u < 8; ++u) {
         if (cb + u < p.nchunks) {
           const int sh = hp.shift[cb + u];
+          if (sh) {  // uniform branch: a new diagonal starts
 #pragma unroll
-          for (int e = 0; e < 4; ++e) hilo_shift(hi[e], lo[e], sh);
+            for (int e = 0; e < 4; ++e) hilo_shift(hi[e], lo[e], sh);
+          }
           hilo_add(hi[0], lo[0], s[u].x);
           hilo_add(hi[1], lo[1], s[u].y);
           hilo_add(hi[2], lo[2], s[u].z);

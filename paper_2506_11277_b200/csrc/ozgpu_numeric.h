@@ -274,39 +274,54 @@ OZ_HD double round_i128(unsigned __int128 v, long e) {
   return neg ? -r : r;
 }
 
+// The rare path of round_hilo, kept out of line so the combine kernel's
+// common path stays small in registers.
+#ifdef __CUDACC__
+static __host__ __device__ __noinline__
+#else
+static inline
+#endif
+double round_hilo_slow(uint64_t hi, uint64_t lo, long e) {
+  const unsigned __int128 v = (static_cast<unsigned __int128>(hi) << 64) | lo;
+  return round_i128(v, e);
+}
+
 // 2^x as a double, x in [-1022, 1023] (normal range only).
 OZ_HD double pow2_normal(long x) { return bits_dbl(static_cast<uint64_t>(x + 1023) << 52); }
 
 // RN(v * 2^e) for the signed 128-bit value v = hi * 2^64 + lo (lo unsigned)
 // -- the same result as round_i128 (and so ExactValue::to_double,
-// oracle.cpp:157-180) but with two exact conversions and one IEEE add on the
-// common path:
-//   v = H + L with H = hi * 2^64 (exact in a double while |hi| < 2^53) and
-//   L = lo.  Rounding L to odd at granularity 2^11, L' = ((lo >> 11) | sticky)
-//   * 2^11, is exact in a double (53 bits) and commutes with adding H (a
-//   multiple of 2^12).  When |v| >= 2^65 (hi >= 2 or hi <= -3) the result's
-//   ulp is >= 2^13 = 4 * 2^11, so RN(H + L') == RN(v) (round-to-odd with two
-//   extra bits, Boldo-Melquiond), and the IEEE add of the two exact scaled
-//   terms rounds once.  The scale 2^e is applied to both terms exactly while
-//   -1033 <= e <= 900 (no subnormal or overflowing intermediate, result
-//   normal).  Everything else takes round_i128.
+// oracle.cpp:157-180) but with two exact conversions and one rounding IEEE
+// operation on the common path:
+//   v = H + L with H = hi * 2^64 and L = lo.  Rounding L to odd at
+//   granularity 2^12, L' = ((lo >> 12) | sticky) * 2^12, commutes with adding
+//   H (a multiple of 2^13).  When |v| >= 2^66 (hi >= 4 or hi <= -5) the
+//   result's ulp is >= 2^14 = 4 * 2^12, so RN(H + L') == RN(v) (round-to-odd
+//   with two extra bits, Boldo-Melquiond).  hi (|hi| < 2^51) and lo >> 12
+//   (52 bits) convert exactly with the 2^52 magic-number trick on the FP64
+//   pipe (no integer->double conversion unit), the scale 2^e is applied to
+//   both terms exactly while -1034 <= e <= 900, and one FMA rounds once.
+//   Everything else takes round_i128.
 OZ_HD double round_hilo(uint64_t hi, uint64_t lo, long e) {
   const int64_t h = static_cast<int64_t>(hi);
-  const bool big = (h >= 2 || h <= -3) && h < (int64_t{1} << 53) && h > -(int64_t{1} << 53);
-  if (big && e >= -1033 && e <= 900) {
+  const bool big = (h >= 4 || h <= -5) && h < (int64_t{1} << 51) && h > -(int64_t{1} << 51);
+  if (big && e >= -1034 && e <= 900) {
+    const uint64_t lr = (lo >> 12) | ((lo & 0xFFF) != 0);
+    // exact: 0x1.8p52 + h and 0x1p52 + lr are representable, their
+    // differences with the magic constants are exact
 #ifdef __CUDA_ARCH__
-    const double hf = __dmul_rn(__ll2double_rn(h), pow2_normal(64 + e));
-    const double lf = __dmul_rn(__ull2double_rn((lo >> 11) | ((lo & 0x7FF) != 0)),
-                                pow2_normal(11 + e));
-    return __dadd_rn(hf, lf);
+    const double hf = __dsub_rn(bits_dbl(0x4338000000000000ULL + static_cast<uint64_t>(h)),
+                                6755399441055744.0);
+    const double lf = __dsub_rn(bits_dbl(0x4330000000000000ULL | lr), 4503599627370496.0);
+    return __fma_rn(hf, pow2_normal(64 + e), __dmul_rn(lf, pow2_normal(12 + e)));
 #else
-    const double hf = static_cast<double>(h) * pow2_normal(64 + e);
-    const double lf = static_cast<double>((lo >> 11) | ((lo & 0x7FF) != 0)) * pow2_normal(11 + e);
-    return hf + lf;
+    const double hf = bits_dbl(0x4338000000000000ULL + static_cast<uint64_t>(h)) -
+                      6755399441055744.0;
+    const double lf = bits_dbl(0x4330000000000000ULL | lr) - 4503599627370496.0;
+    return __builtin_fma(hf, pow2_normal(64 + e), lf * pow2_normal(12 + e));
 #endif
   }
-  const unsigned __int128 v = (static_cast<unsigned __int128>(hi) << 64) | lo;
-  return round_i128(v, e);
+  return round_hilo_slow(hi, lo, e);
 }
 
 }  // namespace ozgpu

@@ -69,12 +69,12 @@ __device__ __forceinline__ void emit_slices8(const double* v, int q, int width, 
 template <typename OutT>
 __global__ void __launch_bounds__(256) slice_rows_kernel(const double* __restrict__ a,
                                                          int64_t lda, int64_t m, int64_t k,
-                                                         int64_t kp, int width, int count,
+                                                         int64_t kp, int64_t plane, int width,
+                                                         int count,
                                                          int mode, OutT* __restrict__ out,
                                                          int* __restrict__ scales,
                                                          int* __restrict__ status) {
   __shared__ unsigned long long red[8];
-  const int64_t plane = m * kp;
   for (int64_t row = blockIdx.x; row < m; row += gridDim.x) {
     const double* ar = a + row * lda;
     unsigned long long mx = 0;
@@ -143,7 +143,8 @@ __global__ void __launch_bounds__(256) colmax_kernel(const double* __restrict__ 
 // written K-major as out[l][n][kp] (the tcgen05 B operand layout).
 template <typename OutT>
 __global__ void __launch_bounds__(256) slice_cols_kernel(
-    const double* __restrict__ b, int64_t ldb, int64_t k, int64_t n, int64_t kp, int width,
+    const double* __restrict__ b, int64_t ldb, int64_t k, int64_t n, int64_t kp, int64_t plane,
+    int width,
     int count, int mode, const unsigned long long* __restrict__ colmax, OutT* __restrict__ out,
     int* __restrict__ scales) {
   __shared__ double tile[64][65];
@@ -157,7 +158,6 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(
   __syncthreads();
   if (blockIdx.x == 0 && threadIdx.x < 64 && n0 + threadIdx.x < n)
     scales[n0 + threadIdx.x] = scale_from_maxbits(colmax[n0 + threadIdx.x]);
-  const int64_t plane = n * kp;
   for (int item = threadIdx.x; item < 64 * 8; item += blockDim.x) {
     int nl = item >> 3, g = item & 7;
     int64_t col = n0 + nl;
@@ -238,11 +238,10 @@ __device__ __forceinline__ void emit8_trunc_i8(const double (&v)[8], int q, int 
 // 8 consecutive entries per lane (the second read of the row hits L2).
 template <int T, bool VEC>
 __global__ void __launch_bounds__(256) slice_rows_fast_kernel(
-    const double* __restrict__ a, int64_t lda, int64_t m, int64_t k, int64_t kp, int count,
-    int8_t* __restrict__ out, int* __restrict__ scales, int* __restrict__ status) {
+    const double* __restrict__ a, int64_t lda, int64_t m, int64_t k, int64_t kp, int64_t plane,
+    int count, int8_t* __restrict__ out, int* __restrict__ scales, int* __restrict__ status) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-  const int64_t plane = m * kp;
   for (int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
        row < m; row += warps) {
     const double* ar = a + row * lda;
@@ -362,11 +361,10 @@ __global__ void __launch_bounds__(256) rowmax_kernel(const double* __restrict__ 
 
 template <int T, bool VEC>
 __global__ void __launch_bounds__(256) slice_rows_stream_kernel(
-    const double* __restrict__ a, int64_t lda, int64_t m, int64_t k, int64_t kp, int count,
-    const int* __restrict__ scales, int8_t* __restrict__ out) {
+    const double* __restrict__ a, int64_t lda, int64_t m, int64_t k, int64_t kp, int64_t plane,
+    int count, const int* __restrict__ scales, int8_t* __restrict__ out) {
   const int64_t groups = kp / 8;
   const int64_t total = m * groups;
-  const int64_t plane = m * kp;
   for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
        idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t row = idx / groups, g = idx - row * groups;
@@ -394,7 +392,8 @@ __global__ void __launch_bounds__(256) slice_rows_stream_kernel(
 // both the row-wise fill and the 8-entry column reads are conflict-light.
 template <int T>
 __global__ void __launch_bounds__(256) slice_cols_fast_kernel(
-    const double* __restrict__ b, int64_t ldb, int64_t k, int64_t n, int64_t kp, int count,
+    const double* __restrict__ b, int64_t ldb, int64_t k, int64_t n, int64_t kp, int64_t plane,
+    int count,
     const unsigned long long* __restrict__ colmax, int8_t* __restrict__ out,
     int* __restrict__ scales) {
   constexpr int TK = 128, TN = 32, STRIDE = TK + 2;  // doubles per column (padded)
@@ -414,7 +413,6 @@ __global__ void __launch_bounds__(256) slice_cols_fast_kernel(
   if (blockIdx.x == 0 && threadIdx.x < TN && n0 + threadIdx.x < n)
     scales[n0 + threadIdx.x] = scale_from_maxbits(colmax[n0 + threadIdx.x]);
   __syncthreads();
-  const int64_t plane = n * kp;
   // item = (column, group of 8 rows); groups fastest so a warp writes 2
   // columns x 128 contiguous bytes per slice
   for (int item = threadIdx.x; item < TN * (TK / 8); item += blockDim.x) {
@@ -441,54 +439,58 @@ static inline int grid_for(int64_t work, int per_block, int cap = 148 * 16) {
 
 template <int T>
 static void launch_rows_fast_t(const double* a, int64_t lda, int64_t m, int64_t k, int64_t kp,
-                               int count, int8_t* out, int* scales, int* status, cudaStream_t st) {
+                               int64_t plane, int count, int8_t* out, int* scales, int* status,
+                               cudaStream_t st) {
   const bool vec = (reinterpret_cast<uintptr_t>(a) & 15) == 0 && (lda & 1) == 0;
   const int grid = grid_for(m, 8, 148 * 16);
   const int grid2 = grid_for(m * (kp / 8), 256, 148 * 16);
   if (vec) {
     rowmax_kernel<true><<<grid, 256, 0, st>>>(a, lda, m, k, scales, status);
-    slice_rows_stream_kernel<T, true><<<grid2, 256, 0, st>>>(a, lda, m, k, kp, count, scales,
-                                                             out);
+    slice_rows_stream_kernel<T, true><<<grid2, 256, 0, st>>>(a, lda, m, k, kp, plane, count,
+                                                             scales, out);
   } else {
     rowmax_kernel<false><<<grid, 256, 0, st>>>(a, lda, m, k, scales, status);
-    slice_rows_stream_kernel<T, false><<<grid2, 256, 0, st>>>(a, lda, m, k, kp, count, scales,
-                                                              out);
+    slice_rows_stream_kernel<T, false><<<grid2, 256, 0, st>>>(a, lda, m, k, kp, plane, count,
+                                                              scales, out);
   }
 }
 
 template <int T>
 static void launch_cols_fast_t(const double* b, int64_t ldb, int64_t k, int64_t n, int64_t kp,
-                               int count, const unsigned long long* colmax, int8_t* out,
-                               int* scales, cudaStream_t st) {
+                               int64_t plane, int count, const unsigned long long* colmax,
+                               int8_t* out, int* scales, cudaStream_t st) {
   dim3 grid(static_cast<unsigned>((kp + 127) / 128), static_cast<unsigned>((n + 31) / 32));
-  slice_cols_fast_kernel<T><<<grid, 256, 0, st>>>(b, ldb, k, n, kp, count, colmax, out, scales);
+  slice_cols_fast_kernel<T><<<grid, 256, 0, st>>>(b, ldb, k, n, kp, plane, count, colmax, out,
+                                                  scales);
 }
 
 cudaError_t launch_slice_rows(const double* a, int64_t lda, int64_t m, int64_t k, int64_t kp,
                               int width, int count, int mode, void* out, int out_is_i64,
-                              int* scales, int* status, cudaStream_t st, int64_t* launches) {
+                              int* scales, int* status, cudaStream_t st, int64_t* launches,
+                              int64_t plane) {
   if (m == 0) return cudaSuccess;
+  if (plane == 0) plane = m * kp;
   if (!out_is_i64 && mode == 0 && width >= 1 && width <= 7) {
     int8_t* o = static_cast<int8_t*>(out);
     switch (width) {
-      case 7: launch_rows_fast_t<7>(a, lda, m, k, kp, count, o, scales, status, st); break;
-      case 6: launch_rows_fast_t<6>(a, lda, m, k, kp, count, o, scales, status, st); break;
-      case 5: launch_rows_fast_t<5>(a, lda, m, k, kp, count, o, scales, status, st); break;
-      case 4: launch_rows_fast_t<4>(a, lda, m, k, kp, count, o, scales, status, st); break;
-      case 3: launch_rows_fast_t<3>(a, lda, m, k, kp, count, o, scales, status, st); break;
-      case 2: launch_rows_fast_t<2>(a, lda, m, k, kp, count, o, scales, status, st); break;
-      default: launch_rows_fast_t<1>(a, lda, m, k, kp, count, o, scales, status, st); break;
+      case 7: launch_rows_fast_t<7>(a, lda, m, k, kp, plane, count, o, scales, status, st); break;
+      case 6: launch_rows_fast_t<6>(a, lda, m, k, kp, plane, count, o, scales, status, st); break;
+      case 5: launch_rows_fast_t<5>(a, lda, m, k, kp, plane, count, o, scales, status, st); break;
+      case 4: launch_rows_fast_t<4>(a, lda, m, k, kp, plane, count, o, scales, status, st); break;
+      case 3: launch_rows_fast_t<3>(a, lda, m, k, kp, plane, count, o, scales, status, st); break;
+      case 2: launch_rows_fast_t<2>(a, lda, m, k, kp, plane, count, o, scales, status, st); break;
+      default: launch_rows_fast_t<1>(a, lda, m, k, kp, plane, count, o, scales, status, st); break;
     }
     *launches += 2;  // rowmax + stream slicing
     return cudaGetLastError();
   }
   int grid = static_cast<int>(m < 148 * 32 ? m : 148 * 32);
   if (out_is_i64)
-    slice_rows_kernel<long long><<<grid, 256, 0, st>>>(a, lda, m, k, kp, width, count, mode,
+    slice_rows_kernel<long long><<<grid, 256, 0, st>>>(a, lda, m, k, kp, plane, width, count, mode,
                                                        static_cast<long long*>(out), scales,
                                                        status);
   else
-    slice_rows_kernel<int8_t><<<grid, 256, 0, st>>>(a, lda, m, k, kp, width, count, mode,
+    slice_rows_kernel<int8_t><<<grid, 256, 0, st>>>(a, lda, m, k, kp, plane, width, count, mode,
                                                     static_cast<int8_t*>(out), scales, status);
   ++*launches;
   return cudaGetLastError();
@@ -497,8 +499,9 @@ cudaError_t launch_slice_rows(const double* a, int64_t lda, int64_t m, int64_t k
 cudaError_t launch_slice_cols(const double* b, int64_t ldb, int64_t k, int64_t n, int64_t kp,
                               int width, int count, int mode, void* out, int out_is_i64,
                               int* scales, unsigned long long* colmax, int* status,
-                              cudaStream_t st, int64_t* launches) {
+                              cudaStream_t st, int64_t* launches, int64_t plane) {
   if (n == 0) return cudaSuccess;
+  if (plane == 0) plane = n * kp;
   cudaError_t e = cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * n, st);
   if (e != cudaSuccess) return e;
   {
@@ -514,24 +517,24 @@ cudaError_t launch_slice_cols(const double* b, int64_t ldb, int64_t k, int64_t n
   if (!out_is_i64 && mode == 0 && width >= 1 && width <= 7 && kp % 128 == 0) {
     int8_t* o = static_cast<int8_t*>(out);
     switch (width) {
-      case 7: launch_cols_fast_t<7>(b, ldb, k, n, kp, count, colmax, o, scales, st); break;
-      case 6: launch_cols_fast_t<6>(b, ldb, k, n, kp, count, colmax, o, scales, st); break;
-      case 5: launch_cols_fast_t<5>(b, ldb, k, n, kp, count, colmax, o, scales, st); break;
-      case 4: launch_cols_fast_t<4>(b, ldb, k, n, kp, count, colmax, o, scales, st); break;
-      case 3: launch_cols_fast_t<3>(b, ldb, k, n, kp, count, colmax, o, scales, st); break;
-      case 2: launch_cols_fast_t<2>(b, ldb, k, n, kp, count, colmax, o, scales, st); break;
-      default: launch_cols_fast_t<1>(b, ldb, k, n, kp, count, colmax, o, scales, st); break;
+      case 7: launch_cols_fast_t<7>(b, ldb, k, n, kp, plane, count, colmax, o, scales, st); break;
+      case 6: launch_cols_fast_t<6>(b, ldb, k, n, kp, plane, count, colmax, o, scales, st); break;
+      case 5: launch_cols_fast_t<5>(b, ldb, k, n, kp, plane, count, colmax, o, scales, st); break;
+      case 4: launch_cols_fast_t<4>(b, ldb, k, n, kp, plane, count, colmax, o, scales, st); break;
+      case 3: launch_cols_fast_t<3>(b, ldb, k, n, kp, plane, count, colmax, o, scales, st); break;
+      case 2: launch_cols_fast_t<2>(b, ldb, k, n, kp, plane, count, colmax, o, scales, st); break;
+      default: launch_cols_fast_t<1>(b, ldb, k, n, kp, plane, count, colmax, o, scales, st); break;
     }
     ++*launches;
     return cudaGetLastError();
   }
   dim3 grid2(static_cast<unsigned>((kp + 63) / 64), static_cast<unsigned>((n + 63) / 64));
   if (out_is_i64)
-    slice_cols_kernel<long long><<<grid2, 256, 0, st>>>(b, ldb, k, n, kp, width, count, mode,
+    slice_cols_kernel<long long><<<grid2, 256, 0, st>>>(b, ldb, k, n, kp, plane, width, count, mode,
                                                         colmax, static_cast<long long*>(out),
                                                         scales);
   else
-    slice_cols_kernel<int8_t><<<grid2, 256, 0, st>>>(b, ldb, k, n, kp, width, count, mode,
+    slice_cols_kernel<int8_t><<<grid2, 256, 0, st>>>(b, ldb, k, n, kp, plane, width, count, mode,
                                                      colmax, static_cast<int8_t*>(out), scales);
   ++*launches;
   return cudaGetLastError();

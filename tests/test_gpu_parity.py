@@ -239,8 +239,8 @@ GEMM_VARIANTS = {
     "cta_pair": {"OZGPU_EPILOGUE": "split", "OZGPU_CTA_PAIR": "1"},
     "bins": {"OZGPU_BINS": "1"},
     "no_bins": {"OZGPU_BINS": "0"},
-    "multicast": {"OZGPU_MC": "1"},
-    "multicast_bins": {"OZGPU_MC": "1", "OZGPU_BINS": "1"},
+    "no_multicast": {"OZGPU_MC": "0"},
+    "no_multicast_bins": {"OZGPU_MC": "0", "OZGPU_BINS": "1"},
     "horner_combine": {"OZGPU_COMBINE": "horner"},
 }
 
@@ -347,3 +347,24 @@ def test_error_bound_matches_reference_and_contains(oz, ref):
         exact = ref.ref_exact_gemm(a, b)
         assert (np.abs(c - exact) <= rep.bound).all()
     assert oz.kappa(a, oz.BlockOrientation.ROWS) == ref.ref_scaling_profile(a, b)[0]
+
+
+@pytest.mark.parametrize("rows,panels,last", [("4", "2", "2"), ("3", "4", "3"), ("8", "1", "1")])
+def test_blocked_host_pipeline_is_bitwise_identical(oz, rows, panels, last, monkeypatch):
+    """ozgpu_dgemm's blocked H2D / compute / D2H pipeline (row blocks, B
+    column panels for the first block, split last block) returns exactly the
+    unblocked result on a ragged shape, for several blockings."""
+    rng = np.random.default_rng(5)
+    m, k, n = 2600, 1000, 3000
+    a = uniform(m, k, rng)
+    b = random_matrix(k, n, rng, -20, 20, 0.01)
+    cfg = oz.MmaConfig.int8_int32()
+    plan = oz.make_plan(cfg, k, 9, 8)
+    monkeypatch.setenv("OZGPU_PIPE", "0")
+    want = oz.multiply(a, b, cfg, plan).c
+    monkeypatch.setenv("OZGPU_PIPE", "1")
+    monkeypatch.setenv("OZGPU_PIPE_ROWS", rows)
+    monkeypatch.setenv("OZGPU_PIPE_PANELS", panels)
+    monkeypatch.setenv("OZGPU_PIPE_LAST", last)
+    got = oz.multiply(a, b, cfg, plan).c
+    assert bits_equal(got, want), mismatch_report(got, want)
