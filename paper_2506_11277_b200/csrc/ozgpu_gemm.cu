@@ -521,7 +521,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
-  const int tiles = p.tiles_m * p.tiles_n;
 
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs; warp-wide loop, elected issuer) ----------------
@@ -529,11 +528,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int unit = pair; unit < p.total_units; unit += npairs) {
-      const int c = unit / tiles;
-      const TileCoord tc = decode_tile(unit - c * tiles, p);
-      const ChunkDesc cd = p.chunks[c];
+      TileCoord tc;
+      int c0, nc;
+      decode_unit(unit, p, false, tc, c0, nc);
       const int arow = tc.tm * 256 + static_cast<int>(rank) * 128;
       const int brow = tc.tn * kBN + static_cast<int>(rank) * 128;
+      for (int c = c0; c < c0 + nc; ++c) {
+      const ChunkDesc cd = p.chunks[chunk_at(p, c)];
       for (int pr = 0; pr < cd.npairs; ++pr) {
         const int l = cd.l0 + pr;
         const int h = cd.d + 2 - l;
@@ -560,6 +561,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           }
         }
       }
+      }
     }
   } else if (warp == 1 && leader) {
     // ---------------- MMA issuer (leader CTA; warp-wide loop, elected issuer) ----------------
@@ -569,9 +571,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    for (int unit = pair; unit < p.total_units; unit += npairs, ++it) {
-      const int c = unit / tiles;
-      const ChunkDesc cd = p.chunks[c];
+    for (int unit = pair; unit < p.total_units; unit += npairs) {
+      TileCoord tc;
+      int c0, nc;
+      decode_unit(unit, p, false, tc, c0, nc);
+      for (int c = c0; c < c0 + nc; ++c, ++it) {
+      const ChunkDesc cd = p.chunks[chunk_at(p, c)];
       const int acc = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
       mbar_wait(&tempty[acc], aphase ^ 1);
@@ -596,6 +601,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           phase ^= 1;
         }
       }
+      }
     }
   } else if (warp >= 4) {
     // ---------------- epilogue (both CTAs): TMEM -> int32 chunk plane ----------------
@@ -603,9 +609,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     const uint32_t tempty_leader0 = map_to_rank(&tempty[0], 0);
     const uint32_t tempty_leader1 = map_to_rank(&tempty[1], 0);
     int it = 0;
-    for (int unit = pair; unit < p.total_units; unit += npairs, ++it) {
-      const int c = unit / tiles;
-      const TileCoord tc = decode_tile(unit - c * tiles, p);
+    for (int unit = pair; unit < p.total_units; unit += npairs) {
+      TileCoord tc;
+      int c0, nc;
+      decode_unit(unit, p, false, tc, c0, nc);
+      for (int cpos = c0; cpos < c0 + nc; ++cpos, ++it) {
+      const int c = chunk_at(p, cpos);
       const int acc = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
       mbar_wait(&tfull[acc], aphase);
@@ -634,6 +643,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+      }
     }
   }
 

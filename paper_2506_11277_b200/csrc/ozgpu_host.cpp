@@ -552,6 +552,20 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
     if (pair) {
       g.tiles_m = static_cast<int>((m + 255) / 256);
       g.total_units = pair_tiles * g.nchunks;
+      bool bins = static_cast<int64_t>(pair_tiles) * g.nchunks >= 2 * static_cast<int64_t>(ctx->num_sms);
+      if (const char* env = std::getenv("OZGPU_BINS")) bins = std::string(env) == "1";
+      std::vector<int>& aux = ctx->host_aux;
+      std::vector<int> bfirst;
+      if (bins && build_bins(cp.chunks, aux, bfirst)) {
+        const size_t nb = bfirst.size() - 1;
+        aux.insert(aux.end(), bfirst.begin(), bfirst.end());
+        int* daux = static_cast<int*>(ctx->aux.get(sizeof(int) * aux.size()));
+        OZ_CUDA(cudaMemcpyAsync(daux, aux.data(), sizeof(int) * aux.size(),
+                                cudaMemcpyHostToDevice, st));
+        g.proc_order = daux;
+        g.bin_first = daux + g.nchunks;
+        g.total_units = static_cast<int>(static_cast<int64_t>(pair_tiles) * nb);
+      }
       CUtensorMap tmb2 = make_slice_map(ctx, slB, kp, n, sb, 128, plane_b);
       OZ_CUDA(launch_gemm_i8_pair(&tma, &tmb2, g, ctx->num_sms, st, &launches));
     } else {

@@ -237,6 +237,7 @@ GEMM_VARIANTS = {
     "final": {"OZGPU_EPILOGUE": "final"},
     "fused": {"OZGPU_EPILOGUE": "fused"},
     "cta_pair": {"OZGPU_EPILOGUE": "split", "OZGPU_CTA_PAIR": "1"},
+    "cta_pair_bins": {"OZGPU_CTA_PAIR": "1", "OZGPU_BINS": "1"},
     "bins": {"OZGPU_BINS": "1"},
     "no_bins": {"OZGPU_BINS": "0"},
     "no_multicast": {"OZGPU_MC": "0"},
