@@ -61,17 +61,23 @@ METRIC = "effective FP64-equiv TFLOP/s (2mnk/t) and int8 tensor-pipe % of peak v
 
 
 def _peaks():
-    """(int8 dense peak TOPS, how) from the driver-measured bf16 cuBLAS rate."""
+    """(int8 dense peak TOPS, its sustained twin, HBM GB/s, how) from the
+    driver-measured bf16 cuBLAS rates (sm_100 int8 dense = 2x bf16 per clock)."""
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
         with open(path) as f:
             mp = json.load(f)
         bf16 = float(mp["bf16_tflops"])
-        return 2.0 * bf16, float(mp.get("hbm_gbs", 6535.4)), \
-            f"2 x measured bf16 cuBLAS burst ({bf16} TFLOP/s, MEASURED_PEAKS.json): sm_100 " \
-            f"int8 dense rate is 2x bf16"
+        sus = float(mp.get("bf16_tflops_sustained", bf16))
+        return 2.0 * bf16, 2.0 * sus, float(mp.get("hbm_gbs", 6535.4)), \
+            f"peak = 2 x measured bf16 cuBLAS burst ({bf16} TFLOP/s, MEASURED_PEAKS.json; " \
+            f"the conservative choice); peak_sustained = 2 x the sustained bf16 rate ({sus}), " \
+            f"the figure for a kernel timed inside a long step.  Unthrottled tcgen05 " \
+            f"kind::i8 issue ceiling measured with tools/ubench/mma_rate.cu: 128 cycles per " \
+            f"128x256x32 MMA (4.6 POPS at 1965 MHz)"
     except Exception:
-        return 2.0 * 1590.0, 6650.0, "2 x fallback bf16 1.59 PFLOP/s (B200_PROFILING.md)"
+        return 2.0 * 1590.0, 2.0 * 1590.0, 6650.0, \
+            "2 x fallback bf16 1.59 PFLOP/s (B200_PROFILING.md)"
 
 
 def _traffic(workload: str):
@@ -346,7 +352,7 @@ def main():
     gemm_ms_call = gemm_ms / max(calls, 1)
     int8_ops = 2.0 * chi * m * n * k
     tops = int8_ops / (gemm_ms_call * 1e-3) / 1e12
-    peak, hbm_peak, peak_how = _peaks()
+    peak, peak_sus, hbm_peak, peak_how = _peaks()
     slice_bytes = 8.0 * (m * k + k * n) + slices[0] * m * k + slices[1] * k * n + 4.0 * (m + n)
     slice_ms_call = slice_ms / max(calls, 1)
 
@@ -368,7 +374,9 @@ def main():
                      "combine": comb_ms / max(calls, 1)},
         "roofline": {"bound": "tensor", "achieved": tops, "peak": peak, "unit": "TFLOP/s",
                      "frac": tops / peak, "traffic": _traffic(args.config),
-                     "kernel": "gemm_i8_kernel (tcgen05.mma kind::i8)",
+                     "peak_sustained": peak_sus, "frac_sustained": tops / peak_sus,
+                     "kernel": "gemm_i8_kernel<0,true> (tcgen05.mma kind::i8, B-multicast "
+                               "2-CTA clusters)",
                      "algorithmic": "2*chi*m*n*k int8 ops per launch", "peak_note": peak_how},
         "slicing_roofline": {"bound": "hbm", "achieved": slice_bytes / (slice_ms_call * 1e-3) / 1e9,
                              "peak": hbm_peak, "unit": "GB/s",

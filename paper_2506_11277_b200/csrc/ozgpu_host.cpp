@@ -536,7 +536,11 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
       return nullptr;
     }
     const int64_t ldp = round_up(n, 4);
-    const int64_t plane = m * ldp;
+    // chunk planes are skewed by 4352 bytes so the combine's concurrent
+    // per-plane streams do not sit a power of two apart (OZGPU_PLANE_SKEW ints)
+    int64_t skew = 1088;
+    if (const char* env = std::getenv("OZGPU_PLANE_SKEW")) skew = std::atoll(env) & ~int64_t{3};
+    const int64_t plane = m * ldp + skew;
     int32_t* planes = static_cast<int32_t*>(
         ctx->planes.get(sizeof(int32_t) * static_cast<size_t>(plane) * cp.chunks.size()));
     g.planes = planes;

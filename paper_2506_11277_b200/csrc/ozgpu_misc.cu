@@ -262,31 +262,51 @@ __global__ void __launch_bounds__(256) combine_horner2_v4_kernel(const CombineAr
   }
 }
 
-// 128-bit Horner combine on (hi, lo) word pairs: per chunk (diagonal-major
-// order) V = (V << shift_c) + S_c with constant-cost funnel shifts (shift_c =
-// t times the diagonal step, < 64) and a carry-chained add, then round_hilo
-// (two exact conversions + one IEEE add on the common path).  About a third
-// of the instructions of the __int128 Horner kernels, so it streams the
-// chunk planes at HBM rate instead of being issue-bound.
+// Exact combine, Horner form with the arithmetic split across pipes:
+// diagonals are accumulated in int64 runs, a = a * 2^(t gap) + S_c, as two
+// integer multiply-adds on the FMA pipe (mad.wide.u32 + mad.lo.u32, the
+// chunk value as the 64-bit addend), and a run is folded into the 128-bit
+// (hi, lo) value with a funnel shift and a carry-chained add on the ALU only
+// every few diagonals; the final rounding (round_hilo) is two exact
+// conversions and one FMA on the FP64 pipe.  A host-built program gives, per
+// chunk (diagonal-major order), the fold and multiply shifts (uniform
+// branches).  The integer pipe was the limiter of the plain 128-bit Horner.
 struct HiloProgram {
-  int shift[64];
-  int final_shift;
+  int fold_shift[64];  // > 0: before chunk c, V = (V << (fold_shift - 1)) + a, a = 0
+  int mul_shift[64];   // a = a * 2^mul_shift + S_c
+  int end_shift;       // after the last chunk: V = (V << end_shift) + a
+  int final_shift;     // then V <<= final_shift (empty trailing diagonals)
 };
 
 __device__ __forceinline__ void hilo_shift(uint64_t& hi, uint64_t& lo, int sh) {
-  // 0 <= sh < 64 (sh == 0: unchanged)
-  hi = sh ? (hi << sh) | (lo >> (64 - sh)) : hi;
+  // 0 < sh < 64
+  hi = (hi << sh) | (lo >> (64 - sh));
   lo = lo << sh;
 }
-__device__ __forceinline__ void hilo_add(uint64_t& hi, uint64_t& lo, int32_t s) {
-  const int64_t s64 = s;
+__device__ __forceinline__ void hilo_add64(uint64_t& hi, uint64_t& lo, int64_t a) {
   asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;"
       : "+l"(lo), "+l"(hi)
-      : "l"(static_cast<uint64_t>(s64)), "l"(static_cast<uint64_t>(s64 >> 63)));
+      : "l"(static_cast<uint64_t>(a)), "l"(static_cast<uint64_t>(a >> 63)));
+}
+// a * r + s (r < 2^32) on the FMA pipe
+__device__ __forceinline__ int64_t mad_run(int64_t a, uint32_t r, int32_t s) {
+  uint64_t res;
+  asm("{\n\t.reg .u32 alo, ahi, shi, rlo, rhi;\n\t"
+      "mov.b64 {alo, ahi}, %1;\n\t"
+      "shr.s32 shi, %3, 31;\n\t"
+      "mov.b64 %0, {%3, shi};\n\t"
+      "mad.wide.u32 %0, alo, %2, %0;\n\t"
+      "mov.b64 {rlo, rhi}, %0;\n\t"
+      "mad.lo.u32 rhi, ahi, %2, rhi;\n\t"
+      "mov.b64 %0, {rlo, rhi};\n\t}"
+      : "=l"(res)
+      : "l"(a), "r"(r), "r"(s));
+  return static_cast<int64_t>(res);
 }
 
-__global__ void __launch_bounds__(256, 3) combine_hilo_v4_kernel(const CombineArgs p,
-                                                                 const HiloProgram hp) {
+template <int BATCH, int MINB>
+__global__ void __launch_bounds__(256, MINB) combine_hilo_v4_kernel(const CombineArgs p,
+                                                                    const HiloProgram hp) {
   const int64_t groups_per_row = p.n / 4;
   const int64_t total = static_cast<int64_t>(p.m) * groups_per_row;
   const bool vec_c = (p.ldc & 1) == 0 && (reinterpret_cast<uintptr_t>(p.c) & 15) == 0;
@@ -296,28 +316,38 @@ __global__ void __launch_bounds__(256, 3) combine_hilo_v4_kernel(const CombineAr
     const int64_t i = idx / groups_per_row, j = (idx - i * groups_per_row) * 4;
     const int4* src = reinterpret_cast<const int4*>(p.planes + i * p.ldp + j);
     uint64_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
-    for (int cb = 0; cb < p.nchunks; cb += 8) {
-      int4 s[8];
+    int64_t a[4] = {0, 0, 0, 0};
+    for (int cb = 0; cb < p.nchunks; cb += BATCH) {
+      int4 s[BATCH];
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < BATCH; ++u)
         if (cb + u < p.nchunks) s[u] = __ldcs(src + (cb + u) * stride4);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < BATCH; ++u) {
         if (cb + u < p.nchunks) {
-          const int sh = hp.shift[cb + u];
-          if (sh) {  // uniform branch: a new diagonal starts
+          const int fs = hp.fold_shift[cb + u];
+          if (fs) {  // uniform branch
 #pragma unroll
-            for (int e = 0; e < 4; ++e) hilo_shift(hi[e], lo[e], sh);
+            for (int e = 0; e < 4; ++e) {
+              if (fs > 1) hilo_shift(hi[e], lo[e], fs - 1);
+              hilo_add64(hi[e], lo[e], a[e]);
+              a[e] = 0;
+            }
           }
-          hilo_add(hi[0], lo[0], s[u].x);
-          hilo_add(hi[1], lo[1], s[u].y);
-          hilo_add(hi[2], lo[2], s[u].z);
-          hilo_add(hi[3], lo[3], s[u].w);
+          const uint32_t r = 1u << hp.mul_shift[cb + u];
+          a[0] = mad_run(a[0], r, s[u].x);
+          a[1] = mad_run(a[1], r, s[u].y);
+          a[2] = mad_run(a[2], r, s[u].z);
+          a[3] = mad_run(a[3], r, s[u].w);
         }
       }
     }
 #pragma unroll
-    for (int e = 0; e < 4; ++e) hilo_shift(hi[e], lo[e], hp.final_shift);
+    for (int e = 0; e < 4; ++e) {
+      if (hp.end_shift) hilo_shift(hi[e], lo[e], hp.end_shift);
+      hilo_add64(hi[e], lo[e], a[e]);
+      if (hp.final_shift) hilo_shift(hi[e], lo[e], hp.final_shift);
+    }
     const long qi = static_cast<long>(__ldg(p.qa + i)) + p.w_last;
     const int4 qb = __ldg(reinterpret_cast<const int4*>(p.qb + j));
     double r[4];
@@ -577,14 +607,51 @@ cudaError_t launch_combine_exact(const CombineArgs& args, int words, const Chunk
       const int grid = grid_for(total / 4, 256, 148 * 8);
       const char* hv = std::getenv("OZGPU_COMBINE");
       if (args.nchunks <= 64 && args.width < 64 && !(hv && std::string(hv) == "horner")) {
+        // runs: an int64 run may span run_bits_max bits above one chunk value
+        // (31 bits) plus the chunk-count growth of a diagonal, sign included
+        int maxc2 = 1;
+        for (int d = 0; d < args.diagonals; ++d)
+          maxc2 = std::max(maxc2, dt.first_chunk[d + 1] - dt.first_chunk[d]);
+        int lg2 = 0;
+        while ((1 << lg2) < maxc2) ++lg2;
+        const int run_bits_max = 30 - lg2;
         HiloProgram hp{};
-        for (int c = 1; c < args.nchunks; ++c)
-          hp.shift[c] = (host_chunks[c].d - host_chunks[c - 1].d) * args.width;
-        hp.final_shift = (args.diagonals - 1 - host_chunks[args.nchunks - 1].d) * args.width;
-        bool ok = hp.final_shift < 64;
-        for (int c = 1; c < args.nchunks; ++c) ok &= hp.shift[c] < 64;
+        bool ok = run_bits_max >= 0;
+        int vd = host_chunks[0].d, run_bits = 0;
+        for (int c = 1; c < args.nchunks && ok; ++c) {
+          const int gap = host_chunks[c].d - host_chunks[c - 1].d;
+          if (gap == 0) continue;
+          if (run_bits + gap * args.width <= run_bits_max && gap * args.width < 32) {
+            hp.mul_shift[c] = gap * args.width;
+            run_bits += gap * args.width;
+          } else {
+            // fold the run (aligned at d_{c-1}) into V (aligned at vd); the
+            // gap to d_c is covered by the next fold, measured from d_{c-1}
+            hp.fold_shift[c] = 1 + (host_chunks[c - 1].d - vd) * args.width;
+            vd = host_chunks[c - 1].d;
+            run_bits = 0;
+            hp.mul_shift[c] = 0;
+          }
+        }
+        const int dl = host_chunks[args.nchunks - 1].d;
+        hp.end_shift = (dl - vd) * args.width;
+        hp.final_shift = (args.diagonals - 1 - dl) * args.width;
+        for (int c = 0; c < args.nchunks; ++c)
+          ok &= hp.fold_shift[c] >= 0 && hp.fold_shift[c] <= 64 && hp.mul_shift[c] < 32;
+        ok &= hp.end_shift < 64 && hp.final_shift < 64;
         if (ok) {
-          combine_hilo_v4_kernel<<<grid, 256, 0, st>>>(args, hp);
+          const char* cv = std::getenv("OZGPU_COMBINE_CFG");
+          const int cfg = cv ? std::atoi(cv) : 44;
+          if (cfg == 84)
+            combine_hilo_v4_kernel<8, 4><<<grid, 256, 0, st>>>(args, hp);
+          else if (cfg == 44)
+            combine_hilo_v4_kernel<4, 4><<<grid, 256, 0, st>>>(args, hp);
+          else if (cfg == 63)
+            combine_hilo_v4_kernel<6, 4><<<grid, 256, 0, st>>>(args, hp);
+          else if (cfg == 122)
+            combine_hilo_v4_kernel<12, 2><<<grid, 256, 0, st>>>(args, hp);
+          else
+            combine_hilo_v4_kernel<8, 3><<<grid, 256, 0, st>>>(args, hp);
           ++*launches;
           return cudaGetLastError();
         }

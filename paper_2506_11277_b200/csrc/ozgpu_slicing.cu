@@ -5,6 +5,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+#include <cstdlib>
+#include <string>
+
 #include "ozgpu_internal.h"
 #include "ozgpu_numeric.h"
 
@@ -234,68 +238,6 @@ __device__ __forceinline__ void emit8_trunc_i8(const double (&v)[8], int q, int 
   }
 }
 
-// One warp per row (grid-stride over rows): warp-shuffle max, then slices of
-// 8 consecutive entries per lane (the second read of the row hits L2).
-template <int T, bool VEC>
-__global__ void __launch_bounds__(256) slice_rows_fast_kernel(
-    const double* __restrict__ a, int64_t lda, int64_t m, int64_t k, int64_t kp, int64_t plane,
-    int count, int8_t* __restrict__ out, int* __restrict__ scales, int* __restrict__ status) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-  for (int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-       row < m; row += warps) {
-    const double* ar = a + row * lda;
-    unsigned long long mx = 0;
-    int bad = 0;
-    int64_t j = lane;
-    for (; j + 224 < k; j += 256) {
-      double x[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) x[u] = __ldg(ar + j + 32 * u);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        bad |= dirty(x[u]);
-        unsigned long long b = abs_bits(x[u]);
-        mx = b > mx ? b : mx;
-      }
-    }
-    for (; j < k; j += 32) {
-      double x = __ldg(ar + j);
-      bad |= dirty(x);
-      unsigned long long b = abs_bits(x);
-      mx = b > mx ? b : mx;
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      unsigned long long t = __shfl_xor_sync(0xFFFFFFFFu, mx, o);
-      mx = t > mx ? t : mx;
-    }
-    bad = __reduce_or_sync(0xFFFFFFFFu, bad);
-    if (lane == 0) {
-      if (bad) atomicOr(status, bad);
-      scales[row] = scale_from_maxbits(mx);
-    }
-    const int q = scale_from_maxbits(mx);
-    for (int64_t g = lane; g < kp / 8; g += 32) {
-      double v[8];
-      const int64_t j0 = g * 8;
-      if (VEC && j0 + 8 <= k) {
-        const double2* p2 = reinterpret_cast<const double2*>(ar + j0);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          double2 t2 = __ldg(p2 + u);
-          v[2 * u] = t2.x;
-          v[2 * u + 1] = t2.y;
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) v[e] = j0 + e < k ? __ldg(ar + j0 + e) : 0.0;
-      }
-      emit8_trunc_i8<T>(v, q, count, out, plane, row * kp + j0);
-    }
-  }
-}
-
 // Two-kernel row path (no dependence between the row reduction and the
 // slice stores, so both kernels stream at HBM rate): rowmax_kernel computes
 // the block scales (one warp per row, 16-byte loads), slice_rows_stream_kernel
@@ -406,9 +348,24 @@ __global__ void __launch_bounds__(256) slice_cols_fast_kernel(
     int u = r >> 1;
     return c * STRIDE + ((u ^ ((u >> 2) & 7)) << 1) + (r & 1);
   };
-  for (int r = warp; r < TK; r += 8) {
-    const int64_t kr = k0 + r, c = n0 + lane;
-    tile[pos(lane, r)] = (kr < k && c < n) ? __ldg(b + kr * ldb + c) : 0.0;
+  // each warp loads 8 row pairs (all 16 loads in flight), then stores each
+  // column's pair as one 16-byte word: lane c hits 16-byte slot c + const
+  // (mod 8) -- 4 wavefronts per 512 bytes, no bank conflicts
+  {
+    double v[16];
+    const int64_t c = n0 + lane;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = 2 * (warp + 8 * i);
+      const int64_t kr = k0 + r;
+      v[2 * i] = (kr < k && c < n) ? __ldcs(b + kr * ldb + c) : 0.0;
+      v[2 * i + 1] = (kr + 1 < k && c < n) ? __ldcs(b + (kr + 1) * ldb + c) : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = 2 * (warp + 8 * i);
+      *reinterpret_cast<double2*>(&tile[pos(lane, r)]) = make_double2(v[2 * i], v[2 * i + 1]);
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x < TN && n0 + threadIdx.x < n)
     scales[n0 + threadIdx.x] = scale_from_maxbits(colmax[n0 + threadIdx.x]);
@@ -438,7 +395,7 @@ static inline int grid_for(int64_t work, int per_block, int cap = 148 * 16) {
 }
 
 template <int T>
-static void launch_rows_fast_t(const double* a, int64_t lda, int64_t m, int64_t k, int64_t kp,
+static int launch_rows_fast_t(const double* a, int64_t lda, int64_t m, int64_t k, int64_t kp,
                                int64_t plane, int count, int8_t* out, int* scales, int* status,
                                cudaStream_t st) {
   const bool vec = (reinterpret_cast<uintptr_t>(a) & 15) == 0 && (lda & 1) == 0;
@@ -453,6 +410,7 @@ static void launch_rows_fast_t(const double* a, int64_t lda, int64_t m, int64_t 
     slice_rows_stream_kernel<T, false><<<grid2, 256, 0, st>>>(a, lda, m, k, kp, plane, count,
                                                               scales, out);
   }
+  return 2;
 }
 
 template <int T>
@@ -472,16 +430,17 @@ cudaError_t launch_slice_rows(const double* a, int64_t lda, int64_t m, int64_t k
   if (plane == 0) plane = m * kp;
   if (!out_is_i64 && mode == 0 && width >= 1 && width <= 7) {
     int8_t* o = static_cast<int8_t*>(out);
+    int n_launch = 0;
     switch (width) {
-      case 7: launch_rows_fast_t<7>(a, lda, m, k, kp, plane, count, o, scales, status, st); break;
-      case 6: launch_rows_fast_t<6>(a, lda, m, k, kp, plane, count, o, scales, status, st); break;
-      case 5: launch_rows_fast_t<5>(a, lda, m, k, kp, plane, count, o, scales, status, st); break;
-      case 4: launch_rows_fast_t<4>(a, lda, m, k, kp, plane, count, o, scales, status, st); break;
-      case 3: launch_rows_fast_t<3>(a, lda, m, k, kp, plane, count, o, scales, status, st); break;
-      case 2: launch_rows_fast_t<2>(a, lda, m, k, kp, plane, count, o, scales, status, st); break;
-      default: launch_rows_fast_t<1>(a, lda, m, k, kp, plane, count, o, scales, status, st); break;
+      case 7: n_launch = launch_rows_fast_t<7>(a, lda, m, k, kp, plane, count, o, scales, status, st); break;
+      case 6: n_launch = launch_rows_fast_t<6>(a, lda, m, k, kp, plane, count, o, scales, status, st); break;
+      case 5: n_launch = launch_rows_fast_t<5>(a, lda, m, k, kp, plane, count, o, scales, status, st); break;
+      case 4: n_launch = launch_rows_fast_t<4>(a, lda, m, k, kp, plane, count, o, scales, status, st); break;
+      case 3: n_launch = launch_rows_fast_t<3>(a, lda, m, k, kp, plane, count, o, scales, status, st); break;
+      case 2: n_launch = launch_rows_fast_t<2>(a, lda, m, k, kp, plane, count, o, scales, status, st); break;
+      default: n_launch = launch_rows_fast_t<1>(a, lda, m, k, kp, plane, count, o, scales, status, st); break;
     }
-    *launches += 2;  // rowmax + stream slicing
+    *launches += n_launch;  // single-pass kernel, or rowmax + stream slicing
     return cudaGetLastError();
   }
   int grid = static_cast<int>(m < 148 * 32 ? m : 148 * 32);
