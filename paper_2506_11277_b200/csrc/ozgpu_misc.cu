@@ -278,15 +278,26 @@ struct HiloProgram {
   int final_shift;     // then V <<= final_shift (empty trailing diagonals)
 };
 
-__device__ __forceinline__ void hilo_shift(uint64_t& hi, uint64_t& lo, int sh) {
-  // 0 < sh < 64
-  hi = (hi << sh) | (lo >> (64 - sh));
-  lo = lo << sh;
+// W-word (W = 2, 3) little-endian two's-complement value: v <<= sh (0 < sh < 64)
+template <int W>
+__device__ __forceinline__ void words_shift(uint64_t (&v)[W], int sh) {
+#pragma unroll
+  for (int i = W - 1; i > 0; --i) v[i] = (v[i] << sh) | (v[i - 1] >> (64 - sh));
+  v[0] <<= sh;
 }
-__device__ __forceinline__ void hilo_add64(uint64_t& hi, uint64_t& lo, int64_t a) {
-  asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;"
-      : "+l"(lo), "+l"(hi)
-      : "l"(static_cast<uint64_t>(a)), "l"(static_cast<uint64_t>(a >> 63)));
+// v += a (sign-extended), one carry chain
+template <int W>
+__device__ __forceinline__ void words_add64(uint64_t (&v)[W], int64_t a) {
+  const uint64_t ext = static_cast<uint64_t>(a >> 63);
+  if constexpr (W == 2) {
+    asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;"
+        : "+l"(v[0]), "+l"(v[1])
+        : "l"(static_cast<uint64_t>(a)), "l"(ext));
+  } else {
+    asm("add.cc.u64 %0, %0, %3;\n\taddc.cc.u64 %1, %1, %4;\n\taddc.u64 %2, %2, %4;"
+        : "+l"(v[0]), "+l"(v[1]), "+l"(v[2])
+        : "l"(static_cast<uint64_t>(a)), "l"(ext));
+  }
 }
 // a * r + s (r < 2^32) on the FMA pipe
 __device__ __forceinline__ int64_t mad_run(int64_t a, uint32_t r, int32_t s) {
@@ -304,7 +315,7 @@ __device__ __forceinline__ int64_t mad_run(int64_t a, uint32_t r, int32_t s) {
   return static_cast<int64_t>(res);
 }
 
-template <int BATCH, int MINB>
+template <int BATCH, int MINB, int W>
 __global__ void __launch_bounds__(256, MINB) combine_hilo_v4_kernel(const CombineArgs p,
                                                                     const HiloProgram hp) {
   const int64_t groups_per_row = p.n / 4;
@@ -315,7 +326,11 @@ __global__ void __launch_bounds__(256, MINB) combine_hilo_v4_kernel(const Combin
        idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t i = idx / groups_per_row, j = (idx - i * groups_per_row) * 4;
     const int4* src = reinterpret_cast<const int4*>(p.planes + i * p.ldp + j);
-    uint64_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
+    uint64_t v[4][W];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+#pragma unroll
+      for (int w = 0; w < W; ++w) v[e][w] = 0;
     int64_t a[4] = {0, 0, 0, 0};
     for (int cb = 0; cb < p.nchunks; cb += BATCH) {
       int4 s[BATCH];
@@ -329,8 +344,8 @@ __global__ void __launch_bounds__(256, MINB) combine_hilo_v4_kernel(const Combin
           if (fs) {  // uniform branch
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              if (fs > 1) hilo_shift(hi[e], lo[e], fs - 1);
-              hilo_add64(hi[e], lo[e], a[e]);
+              if (fs > 1) words_shift<W>(v[e], fs - 1);
+              words_add64<W>(v[e], a[e]);
               a[e] = 0;
             }
           }
@@ -344,17 +359,21 @@ __global__ void __launch_bounds__(256, MINB) combine_hilo_v4_kernel(const Combin
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      if (hp.end_shift) hilo_shift(hi[e], lo[e], hp.end_shift);
-      hilo_add64(hi[e], lo[e], a[e]);
-      if (hp.final_shift) hilo_shift(hi[e], lo[e], hp.final_shift);
+      if (hp.end_shift) words_shift<W>(v[e], hp.end_shift);
+      words_add64<W>(v[e], a[e]);
+      if (hp.final_shift) words_shift<W>(v[e], hp.final_shift);
     }
     const long qi = static_cast<long>(__ldg(p.qa + i)) + p.w_last;
     const int4 qb = __ldg(reinterpret_cast<const int4*>(p.qb + j));
+    const long qe[4] = {qi + qb.x, qi + qb.y, qi + qb.z, qi + qb.w};
     double r[4];
-    r[0] = round_hilo(hi[0], lo[0], qi + qb.x);
-    r[1] = round_hilo(hi[1], lo[1], qi + qb.y);
-    r[2] = round_hilo(hi[2], lo[2], qi + qb.z);
-    r[3] = round_hilo(hi[3], lo[3], qi + qb.w);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if constexpr (W == 2)
+        r[e] = round_hilo(v[e][1], v[e][0], qe[e]);
+      else
+        r[e] = round_w3(v[e][2], v[e][1], v[e][0], qe[e]);
+    }
     if (p.axpby) {  // two roundings, no FMA contraction (scheme.cpp:369-370)
 #pragma unroll
       for (int e = 0; e < 4; ++e)
@@ -582,8 +601,9 @@ cudaError_t launch_combine_exact(const CombineArgs& args, int words, const Chunk
                                  cudaStream_t st, int64_t* launches) {
   int64_t total = static_cast<int64_t>(args.m) * args.n;
   if (total == 0) return cudaSuccess;
-  if (args.n % 4 == 0 && args.ldp % 4 == 0 && words == 2 && args.diagonals <= 64 &&
-      static_cast<int64_t>(args.diagonals - 1) * args.width + 40 <= 126) {
+  const int64_t vbits = static_cast<int64_t>(args.diagonals - 1) * args.width + 40;
+  if (args.n % 4 == 0 && args.ldp % 4 == 0 && args.diagonals <= 64 &&
+      ((words == 2 && vbits <= 126) || (words == 3 && vbits <= 190))) {
     // chunks are stored diagonal-major (build_chunks): tabulate each diagonal's range
     DiagTable dt{};
     int c = 0;
@@ -606,6 +626,7 @@ cudaError_t launch_combine_exact(const CombineArgs& args, int words, const Chunk
       a2.hgroup = std::max(1, 1 + (62 - (31 + lg)) / std::max(1, args.width));
       const int grid = grid_for(total / 4, 256, 148 * 8);
       const char* hv = std::getenv("OZGPU_COMBINE");
+      const bool w3 = vbits > 126;
       if (args.nchunks <= 64 && args.width < 64 && !(hv && std::string(hv) == "horner")) {
         // runs: an int64 run may span run_bits_max bits above one chunk value
         // (31 bits) plus the chunk-count growth of a diagonal, sign included
@@ -640,45 +661,45 @@ cudaError_t launch_combine_exact(const CombineArgs& args, int words, const Chunk
           ok &= hp.fold_shift[c] >= 0 && hp.fold_shift[c] <= 64 && hp.mul_shift[c] < 32;
         ok &= hp.end_shift < 64 && hp.final_shift < 64;
         if (ok) {
+          // 4 chunk loads in flight per batch, 4 CTAs / SM: measured best of
+          // {4,6,8,12} x {2,3,4} on B200 (OZGPU_COMBINE_CFG=83 selects 8 / 3)
           const char* cv = std::getenv("OZGPU_COMBINE_CFG");
           const int cfg = cv ? std::atoi(cv) : 44;
-          if (cfg == 84)
-            combine_hilo_v4_kernel<8, 4><<<grid, 256, 0, st>>>(args, hp);
-          else if (cfg == 44)
-            combine_hilo_v4_kernel<4, 4><<<grid, 256, 0, st>>>(args, hp);
-          else if (cfg == 63)
-            combine_hilo_v4_kernel<6, 4><<<grid, 256, 0, st>>>(args, hp);
-          else if (cfg == 122)
-            combine_hilo_v4_kernel<12, 2><<<grid, 256, 0, st>>>(args, hp);
+          if (w3)
+            combine_hilo_v4_kernel<4, 3, 3><<<grid, 256, 0, st>>>(args, hp);
+          else if (cfg == 83)
+            combine_hilo_v4_kernel<8, 3, 2><<<grid, 256, 0, st>>>(args, hp);
           else
-            combine_hilo_v4_kernel<8, 3><<<grid, 256, 0, st>>>(args, hp);
+            combine_hilo_v4_kernel<4, 4, 2><<<grid, 256, 0, st>>>(args, hp);
           ++*launches;
           return cudaGetLastError();
         }
       }
-      if (args.nchunks <= 64) {
-        HornerProgram hp{};
-        int run_len = 0;
-        for (int c = 0; c < args.nchunks; ++c) {
-          const bool newdiag = c == 0 || host_chunks[c].d != host_chunks[c - 1].d;
-          if (c > 0 && newdiag) {
-            if (run_len == a2.hgroup) {
-              hp.flags[c] = 2;
-              hp.fold_shift[c] = args.width * run_len;
-              run_len = 0;
-            } else {
-              hp.flags[c] = 1;
+      if (!w3) {  // 3-word values without the fast path: generic kernel below
+        if (args.nchunks <= 64) {
+          HornerProgram hp{};
+          int run_len = 0;
+          for (int c = 0; c < args.nchunks; ++c) {
+            const bool newdiag = c == 0 || host_chunks[c].d != host_chunks[c - 1].d;
+            if (c > 0 && newdiag) {
+              if (run_len == a2.hgroup) {
+                hp.flags[c] = 2;
+                hp.fold_shift[c] = args.width * run_len;
+                run_len = 0;
+              } else {
+                hp.flags[c] = 1;
+              }
             }
+            if (newdiag) ++run_len;
           }
-          if (newdiag) ++run_len;
+          hp.final_shift = args.width * run_len;
+          combine_horner2_v4_kernel<<<grid, 256, 0, st>>>(a2, hp);
+        } else {
+          combine_horner_v4_kernel<<<grid, 256, 0, st>>>(a2, dt);
         }
-        hp.final_shift = args.width * run_len;
-        combine_horner2_v4_kernel<<<grid, 256, 0, st>>>(a2, hp);
-      } else {
-        combine_horner_v4_kernel<<<grid, 256, 0, st>>>(a2, dt);
+        ++*launches;
+        return cudaGetLastError();
       }
-      ++*launches;
-      return cudaGetLastError();
     }
   }
   if (args.n % 4 == 0 && args.nchunks <= 64 && args.ldp % 4 == 0 && words <= 3) {

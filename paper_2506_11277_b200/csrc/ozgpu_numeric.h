@@ -324,4 +324,48 @@ OZ_HD double round_hilo(uint64_t hi, uint64_t lo, long e) {
   return round_hilo_slow(hi, lo, e);
 }
 
+// The 192-bit counterpart of round_hilo for v = w2 * 2^128 + w1 * 2^64 + w0
+// (w1, w0 unsigned): values that fit 128 bits go through round_hilo; for
+// |v| >= 2^130 (w2 >= 4 or w2 <= -5) the low 128 bits are rounded to odd at
+// granularity 2^76 (52 bits, exact in a double) and added to w2 * 2^128 with
+// one FMA -- the same argument as round_hilo, two guard bits.  The rest goes
+// through round_words<3>.
+#ifdef __CUDACC__
+static __host__ __device__ __noinline__
+#else
+static inline
+#endif
+double round_w3_rest(uint64_t w2, uint64_t w1, uint64_t w0, long e);
+
+OZ_HD double round_w3(uint64_t w2, uint64_t w1, uint64_t w0, long e) {
+  const int64_t h = static_cast<int64_t>(w2);
+  if (h == (static_cast<int64_t>(w1) >> 63)) return round_hilo(w1, w0, e);
+  const bool big = (h >= 4 || h <= -5) && h < (int64_t{1} << 51) && h > -(int64_t{1} << 51);
+  if (big && e >= -1098 && e <= 844) {
+    const uint64_t lr = (w1 >> 12) | (((w1 & 0xFFF) | w0) != 0);
+#ifdef __CUDA_ARCH__
+    const double hf = __dsub_rn(bits_dbl(0x4338000000000000ULL + static_cast<uint64_t>(h)),
+                                6755399441055744.0);
+    const double lf = __dsub_rn(bits_dbl(0x4330000000000000ULL | lr), 4503599627370496.0);
+    return __fma_rn(hf, pow2_normal(128 + e), __dmul_rn(lf, pow2_normal(76 + e)));
+#else
+    const double hf = bits_dbl(0x4338000000000000ULL + static_cast<uint64_t>(h)) -
+                      6755399441055744.0;
+    const double lf = bits_dbl(0x4330000000000000ULL | lr) - 4503599627370496.0;
+    return __builtin_fma(hf, pow2_normal(128 + e), lf * pow2_normal(76 + e));
+#endif
+  }
+  return round_w3_rest(w2, w1, w0, e);
+}
+
+#ifdef __CUDACC__
+static __host__ __device__ __noinline__
+#else
+static inline
+#endif
+double round_w3_rest(uint64_t w2, uint64_t w1, uint64_t w0, long e) {
+  const uint64_t v[3] = {w0, w1, w2};
+  return round_words<3>(v, e);
+}
+
 }  // namespace ozgpu

@@ -301,8 +301,8 @@ __global__ void __launch_bounds__(256) rowmax_kernel(const double* __restrict__ 
   }
 }
 
-template <int T, bool VEC>
-__global__ void __launch_bounds__(256) slice_rows_stream_kernel(
+template <int T, bool VEC, int MINB>
+__global__ void __launch_bounds__(256, MINB) slice_rows_stream_kernel(
     const double* __restrict__ a, int64_t lda, int64_t m, int64_t k, int64_t kp, int64_t plane,
     int count, const int* __restrict__ scales, int8_t* __restrict__ out) {
   const int64_t groups = kp / 8;
@@ -401,14 +401,20 @@ static int launch_rows_fast_t(const double* a, int64_t lda, int64_t m, int64_t k
   const bool vec = (reinterpret_cast<uintptr_t>(a) & 15) == 0 && (lda & 1) == 0;
   const int grid = grid_for(m, 8, 148 * 16);
   const int grid2 = grid_for(m * (kp / 8), 256, 148 * 16);
+  const char* mb = std::getenv("OZGPU_SLICE_MINB");
+  const bool four = mb && std::atoi(mb) == 4;
   if (vec) {
     rowmax_kernel<true><<<grid, 256, 0, st>>>(a, lda, m, k, scales, status);
-    slice_rows_stream_kernel<T, true><<<grid2, 256, 0, st>>>(a, lda, m, k, kp, plane, count,
-                                                             scales, out);
+    if (four)
+      slice_rows_stream_kernel<T, true, 4><<<grid2, 256, 0, st>>>(a, lda, m, k, kp, plane, count,
+                                                                  scales, out);
+    else
+      slice_rows_stream_kernel<T, true, 1><<<grid2, 256, 0, st>>>(a, lda, m, k, kp, plane, count,
+                                                                  scales, out);
   } else {
     rowmax_kernel<false><<<grid, 256, 0, st>>>(a, lda, m, k, scales, status);
-    slice_rows_stream_kernel<T, false><<<grid2, 256, 0, st>>>(a, lda, m, k, kp, plane, count,
-                                                              scales, out);
+    slice_rows_stream_kernel<T, false, 1><<<grid2, 256, 0, st>>>(a, lda, m, k, kp, plane, count,
+                                                                 scales, out);
   }
   return 2;
 }

@@ -44,3 +44,7 @@ extern "C" double nt_round_i128(uint64_t lo, uint64_t hi, long e) {
 }
 
 extern "C" double nt_round_hilo(uint64_t lo, uint64_t hi, long e) { return round_hilo(hi, lo, e); }
+
+extern "C" double nt_round_w3(uint64_t w0, uint64_t w1, uint64_t w2, long e) {
+  return round_w3(w2, w1, w0, e);
+}

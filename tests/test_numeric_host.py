@@ -182,3 +182,38 @@ def test_round_hilo_fast_path_matches_exact(nt):
         want = _exact_round(v, e)
         assert got == want or (math.isinf(got) and math.isinf(want)), (v, e, got, want)
         assert math.copysign(1, got) == math.copysign(1, want) or want == 0, (v, e)
+
+
+def test_round_w3_matches_exact(nt):
+    """round_w3 (192-bit values: 128-bit path, two-term fast path, generic
+    W-word path) equals ExactValue::to_double on random, boundary and tie
+    cases."""
+    nt.nt_round_w3.restype = ctypes.c_double
+    nt.nt_round_w3.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_long]
+    rng = np.random.default_rng(8)
+    cases = []
+    for trial in range(30000):
+        kind = trial % 4
+        nb = int(rng.integers(1, 180))
+        if kind == 0:
+            v = (int(rng.integers(0, 2**62)) << max(0, nb - 62)) | int(rng.integers(0, 2**30))
+        elif kind == 1:  # around 2^128 .. 2^133 (the fast-path boundary)
+            v = (int(rng.integers(1, 2**5)) << 128) + (int(rng.integers(0, 2**62)) << 64) + \
+                int(rng.integers(0, 2**62))
+        elif kind == 2:  # exact ties at 53 bits
+            nb = int(rng.integers(131, 178))
+            v = (int(rng.integers(2**53, 2**54)) | 1) << (nb - 54)
+            if trial % 8 == 2:
+                v += 1
+        else:  # sticky bit only in the lowest word
+            v = (int(rng.integers(2**10, 2**40)) << 128) + int(rng.integers(0, 3))
+        v &= (1 << 190) - 1
+        if trial % 2:
+            v = -v
+        e = int(rng.integers(-1150, 900)) if trial % 6 == 0 else int(rng.integers(-300, 60))
+        cases.append((v, e))
+    for v, e in cases:
+        u = v % (1 << 192)
+        got = nt.nt_round_w3(u & (2**64 - 1), (u >> 64) & (2**64 - 1), u >> 128, e)
+        want = _exact_round(v, e)
+        assert got == want or (math.isinf(got) and math.isinf(want)), (v, e, got, want)
