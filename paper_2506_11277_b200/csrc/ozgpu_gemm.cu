@@ -28,6 +28,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 #include "ozgpu_internal.h"
 #include "ozgpu_numeric.h"
 #include "ozgpu_ptx.cuh"
@@ -35,7 +37,7 @@
 namespace ozgpu {
 
 constexpr int kBN = 256;
-constexpr int kStages = 4;
+constexpr int kStages = 4;  // 1-CTA kernel default (template parameter)
 constexpr int kABytes = kBlockM * kBlockK;  // 16 KB
 constexpr int kBBytes = kBN * kBlockK;      // 32 KB
 constexpr int kStageBytes = kABytes + kBBytes;
@@ -225,7 +227,7 @@ __device__ __forceinline__ void store_staged(const GemmArgs& p, const double* st
 // and multicasting it to both (L2 -> SM operand traffic 64 KB instead of
 // 96 KB per 2 x 128 x 256 x 128 step).  A stage is refilled only after both
 // CTAs' MMAs released it (empty barriers count 2, commits multicast).
-template <int W, bool MC>
+template <int W, bool MC, int kStages = 4>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_i8_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
                    const GemmArgs p) {
@@ -477,11 +479,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 // epilogue warps of both CTAs release the accumulator on the leader.
 // ----------------------------------------------------------------------------
 
-constexpr int kPairStages = 6;
 constexpr int kPairHalfBytes = 128 * kBlockK;             // 16 KB (A or B half)
 constexpr int kPairStageBytes = 2 * kPairHalfBytes;       // per CTA
-constexpr int kSmemPair = kPairStages * kPairStageBytes + 1024 + 256;
+constexpr int smem_pair(int stages) { return stages * kPairStageBytes + 1024 + 256; }
 
+template <int kPairStages>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     gemm_i8_pair_kernel(const __grid_constant__ CUtensorMap tma,
                         const __grid_constant__ CUtensorMap tmb, const GemmArgs p) {
@@ -633,7 +635,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             int4* d4 = reinterpret_cast<int4*>(dst + col0);
 #pragma unroll
             for (int v = 0; v < 8; ++v)
-              __stcs(d4 + v, make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]));
+              d4[v] = make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
           } else {
             for (int v = 0; v < 32; ++v)
               if (col0 + v < p.n) dst[col0 + v] = static_cast<int32_t>(r[v]);
@@ -655,20 +657,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   }
 }
 
-cudaError_t launch_gemm_i8_pair(const CUtensorMap* tma, const CUtensorMap* tmb,
-                                const GemmArgs& args, int num_sms, cudaStream_t st,
-                                int64_t* launches) {
+template <int S>
+static cudaError_t launch_pair_t(const CUtensorMap* tma, const CUtensorMap* tmb,
+                                 const GemmArgs& args, int pairs, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_i8_pair_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemPair);
+    cudaError_t e = cudaFuncSetAttribute(gemm_i8_pair_kernel<S>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pair(S));
     if (e != cudaSuccess) return e;
     configured = true;
   }
+  gemm_i8_pair_kernel<S><<<2 * pairs, kGemmThreads, smem_pair(S), st>>>(*tma, *tmb, args);
+  return cudaSuccess;
+}
+
+cudaError_t launch_gemm_i8_pair(const CUtensorMap* tma, const CUtensorMap* tmb,
+                                const GemmArgs& args, int num_sms, cudaStream_t st,
+                                int64_t* launches) {
   int pairs = num_sms / 2;
   if (args.total_units < pairs) pairs = args.total_units;
   if (pairs < 1) return cudaSuccess;
-  gemm_i8_pair_kernel<<<2 * pairs, kGemmThreads, kSmemPair, st>>>(*tma, *tmb, args);
+  const char* sv = std::getenv("OZGPU_PAIR_STAGES");
+  const int stages = sv ? std::atoi(sv) : 4;
+  cudaError_t e0 = stages == 6 ? launch_pair_t<6>(tma, tmb, args, pairs, st)
+                 : stages == 5 ? launch_pair_t<5>(tma, tmb, args, pairs, st)
+                 : stages == 3 ? launch_pair_t<3>(tma, tmb, args, pairs, st)
+                               : launch_pair_t<4>(tma, tmb, args, pairs, st);
+  if (e0 != cudaSuccess) return e0;
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) ++*launches;
   return e;
@@ -679,32 +694,30 @@ static cudaError_t launch_t(const CUtensorMap* tma, const CUtensorMap* tmb, cons
                             int grid, int smem, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_i8_kernel<W, false>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_i8_kernel<W, false, 4>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  gemm_i8_kernel<W, false><<<grid, kGemmThreads, smem, st>>>(*tma, *tmb, args);
+  gemm_i8_kernel<W, false, 4><<<grid, kGemmThreads, smem, st>>>(*tma, *tmb, args);
   return cudaGetLastError();
 }
 
-cudaError_t launch_gemm_i8_mc(const CUtensorMap* tma, const CUtensorMap* tmb_half,
-                              const GemmArgs& args, int num_sms, cudaStream_t st,
-                              int64_t* launches) {
+template <int S>
+static cudaError_t launch_mc_t(const CUtensorMap* tma, const CUtensorMap* tmb_half,
+                               const GemmArgs& args, int clusters, cudaStream_t st) {
+  constexpr int smem = S * kStageBytes + 1024 + 256;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_i8_kernel<0, true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSplit);
+    cudaError_t e = cudaFuncSetAttribute(gemm_i8_kernel<0, true, S>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  int clusters = num_sms / 2;
-  if (args.total_units < clusters) clusters = args.total_units;
-  if (clusters < 1) return cudaSuccess;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * clusters);
   cfg.blockDim = dim3(kGemmThreads);
-  cfg.dynamicSmemBytes = kSmemSplit;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -713,7 +726,19 @@ cudaError_t launch_gemm_i8_mc(const CUtensorMap* tma, const CUtensorMap* tmb_hal
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_i8_kernel<0, true>, *tma, *tmb_half, args);
+  return cudaLaunchKernelEx(&cfg, gemm_i8_kernel<0, true, S>, *tma, *tmb_half, args);
+}
+
+cudaError_t launch_gemm_i8_mc(const CUtensorMap* tma, const CUtensorMap* tmb_half,
+                              const GemmArgs& args, int num_sms, cudaStream_t st,
+                              int64_t* launches) {
+  int clusters = num_sms / 2;
+  if (args.total_units < clusters) clusters = args.total_units;
+  if (clusters < 1) return cudaSuccess;
+  const char* sv = std::getenv("OZGPU_MC_STAGES");
+  const int stages = sv ? std::atoi(sv) : 4;
+  cudaError_t e = stages == 3 ? launch_mc_t<3>(tma, tmb_half, args, clusters, st)
+                              : launch_mc_t<4>(tma, tmb_half, args, clusters, st);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) ++*launches;
   return e;

@@ -401,8 +401,9 @@ static int launch_rows_fast_t(const double* a, int64_t lda, int64_t m, int64_t k
   const bool vec = (reinterpret_cast<uintptr_t>(a) & 15) == 0 && (lda & 1) == 0;
   const int grid = grid_for(m, 8, 148 * 16);
   const int grid2 = grid_for(m * (kp / 8), 256, 148 * 16);
+  // 4 CTAs / SM (64 registers, measured ~3% faster than 3 / SM on B200)
   const char* mb = std::getenv("OZGPU_SLICE_MINB");
-  const bool four = mb && std::atoi(mb) == 4;
+  const bool four = !(mb && std::atoi(mb) == 1);
   if (vec) {
     rowmax_kernel<true><<<grid, 256, 0, st>>>(a, lda, m, k, scales, status);
     if (four)
