@@ -166,12 +166,13 @@ CUtensorMapL2promotion l2_promotion() {
 // 3-D int8 tensor map over slices [count][rows][kp], box {128, box_rows, 1},
 // 128-byte swizzle (matches the UMMA SW128 K-major descriptor).
 CUtensorMap make_slice_map(ozgpu_ctx* ctx, const void* base, int64_t kp, int64_t rows,
-                           int count, int box_rows, int64_t plane = 0) {
+                           int count, int box_rows, int64_t plane = 0, int64_t ld = 0) {
   CUtensorMap m;
+  if (ld == 0) ld = kp;
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(kp), static_cast<cuuint64_t>(rows),
                         static_cast<cuuint64_t>(count)};
-  cuuint64_t strides[2] = {static_cast<cuuint64_t>(kp),
-                           static_cast<cuuint64_t>(plane ? plane : kp * rows)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld),
+                           static_cast<cuuint64_t>(plane ? plane : ld * rows)};
   cuuint32_t box[3] = {static_cast<cuuint32_t>(kBlockK), static_cast<cuuint32_t>(box_rows), 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = ctx->encode(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims,
@@ -183,6 +184,15 @@ CUtensorMap make_slice_map(ozgpu_ctx* ctx, const void* base, int64_t kp, int64_t
 }
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// Row stride of the slice buffers: the K extent kp (a multiple of 128) plus
+// an optional pad (OZGPU_KPAD bytes, multiple of 128; the pad is zero-filled
+// by the slicing kernels and never read by the GEMM).
+int64_t slice_ld(int64_t kp) {
+  int64_t pad = 0;
+  if (const char* env = std::getenv("OZGPU_KPAD")) pad = round_up(std::max<int64_t>(0, std::atoll(env)), 128);
+  return kp + pad;
+}
 
 cudaEvent_t take_event(ozgpu_ctx* ctx) {
   if (!ctx->event_pool.empty()) {
@@ -403,6 +413,7 @@ struct Presliced {
   const int8_t* b;
   int64_t plane_b;
   const int* qb;
+  int64_t ld;  // row stride of the slice buffers
 };
 
 // The device-resident core of multiply(): everything is enqueued on `st`.
@@ -426,13 +437,14 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
   if (p.mode == 1 && t < 2) throw std::invalid_argument("split: nearest mode needs width >= 2");
   const int sa = p.slices_a, sb = p.slices_b;
   const int64_t kp = round_up(k, kKPad);
+  const int64_t ld = pre ? pre->ld : slice_ld(kp);
   ChunkPlan cp = build_chunks(p, cfg, k);
 
   const int8_t* slA;
   const int8_t* slB;
   const int* qa;
   const int* qb;
-  int64_t plane_a = m * kp, plane_b = n * kp;
+  int64_t plane_a = m * ld, plane_b = n * ld;
   if (pre) {
     slA = pre->a;
     slB = pre->b;
@@ -441,16 +453,16 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
     plane_a = pre->plane_a;
     plane_b = pre->plane_b;
   } else {
-    int8_t* wa = static_cast<int8_t*>(ctx->slices_a.get(static_cast<size_t>(sa) * m * kp + 1));
-    int8_t* wb = static_cast<int8_t*>(ctx->slices_b.get(static_cast<size_t>(sb) * n * kp + 1));
+    int8_t* wa = static_cast<int8_t*>(ctx->slices_a.get(static_cast<size_t>(sa) * m * ld + 1));
+    int8_t* wb = static_cast<int8_t*>(ctx->slices_b.get(static_cast<size_t>(sb) * n * ld + 1));
     int* wqa = static_cast<int*>(ctx->qa.get(sizeof(int) * (m + 1)));
     int* wqb = static_cast<int*>(ctx->qb.get(sizeof(int) * (n + 1)));
     auto* colmax = static_cast<unsigned long long*>(ctx->colmax.get(8 * (n + 1)));
     int* status = dev_status ? dev_status : static_cast<int*>(ctx->status.get(sizeof(int)));
     OZ_CUDA(cudaMemsetAsync(status, 0, sizeof(int), st));
-    OZ_CUDA(launch_slice_rows(da, lda, m, k, kp, t, sa, p.mode, wa, 0, wqa, status, st,
+    OZ_CUDA(launch_slice_rows(da, lda, m, k, ld, t, sa, p.mode, wa, 0, wqa, status, st,
                               &launches));
-    OZ_CUDA(launch_slice_cols(db, ldb, k, n, kp, t, sb, p.mode, wb, 0, wqb, colmax, status, st,
+    OZ_CUDA(launch_slice_cols(db, ldb, k, n, ld, t, sb, p.mode, wb, 0, wqb, colmax, status, st,
                               &launches));
     slA = wa;
     slB = wb;
@@ -496,8 +508,8 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
                             cudaMemcpyHostToDevice, st));
     ctx->host_chunks = cp.chunks;
 
-    CUtensorMap tma = make_slice_map(ctx, slA, kp, m, sa, kBlockM, plane_a);
-    CUtensorMap tmb = make_slice_map(ctx, slB, kp, n, sb, 256, plane_b);
+    CUtensorMap tma = make_slice_map(ctx, slA, kp, m, sa, kBlockM, plane_a, ld);
+    CUtensorMap tmb = make_slice_map(ctx, slB, kp, n, sb, 256, plane_b, ld);
     GemmArgs g{};
     g.chunks = dchunks;
     g.nchunks = static_cast<int>(cp.chunks.size());
@@ -570,7 +582,7 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
         g.bin_first = daux + g.nchunks;
         g.total_units = static_cast<int>(static_cast<int64_t>(pair_tiles) * nb);
       }
-      CUtensorMap tmb2 = make_slice_map(ctx, slB, kp, n, sb, 128, plane_b);
+      CUtensorMap tmb2 = make_slice_map(ctx, slB, kp, n, sb, 128, plane_b, ld);
       OZ_CUDA(launch_gemm_i8_pair(&tma, &tmb2, g, ctx->num_sms, st, &launches));
     } else {
       g.total_units = static_cast<int>(tiles * g.nchunks);
@@ -655,7 +667,7 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
       if (mc) {
         const int64_t super_tiles = static_cast<int64_t>((tiles_m + 1) / 2) * tiles_n;
         g.total_units = static_cast<int>(g.total_units / tiles * super_tiles);
-        CUtensorMap tmb_half = make_slice_map(ctx, slB, kp, n, sb, 128, plane_b);
+        CUtensorMap tmb_half = make_slice_map(ctx, slB, kp, n, sb, 128, plane_b, ld);
         OZ_CUDA(launch_gemm_i8_mc(&tma, &tmb_half, g, ctx->num_sms, st, &launches));
       } else {
         OZ_CUDA(launch_gemm_i8(&tma, &tmb, g, ctx->num_sms, st, &launches));
@@ -776,7 +788,7 @@ void host_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double
       OZ_CUDA(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
     }
     const int t = p.width;
-    const int64_t kp = round_up(k, kKPad);
+    const int64_t kp = slice_ld(round_up(k, kKPad));  // slice row stride
     double* dc = static_cast<double*>(ctx->io_c.get(sizeof(double) * m * n + 8));
     int8_t* slA =
         static_cast<int8_t*>(ctx->slices_a.get(static_cast<size_t>(p.slices_a) * m * kp + 1));
@@ -846,7 +858,7 @@ void host_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double
       mark("slice A" + std::to_string(i), st);
     };
     auto block = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1) {
-      Presliced pre{slA + r0 * kp, m * kp, qa + r0, slB + c0 * kp, n * kp, qb + c0};
+      Presliced pre{slA + r0 * kp, m * kp, qa + r0, slB + c0 * kp, n * kp, qb + c0, kp};
       run_multiply(ctx, r1 - r0, c1 - c0, k, nullptr, 0, nullptr, 0, dc + r0 * n + c0, n, cfg, p,
                    st, nullptr, false, 1.0, 0.0, nullptr, 0, &pre);
       cudaEvent_t done = next_event();
