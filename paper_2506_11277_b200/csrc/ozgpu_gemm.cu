@@ -140,6 +140,36 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* ptr) {
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
   return v;
 }
+// Wave lockstep (see GemmArgs::sync): called by the whole producer warp at
+// every k-step; returns the (warp-uniform) new lockstep state.  CTAs of a
+// wave share their operand panels through L2 only while they stream them at
+// about the same time, and a deep TMA pipeline hides exactly the misses that
+// would otherwise keep them together -- measured on B200, the drift doubles
+// or triples DRAM reads.  Every sync_g k-steps the cluster publishes its
+// group and waits until all clusters have passed the group sync_d back.
+__device__ __forceinline__ bool lockstep_point(const GemmArgs& p, int step, bool lockstep) {
+  if (!lockstep || step % p.sync_g != 0) return lockstep;
+  if (step >= p.sync_steps) return false;
+  const int g = step / p.sync_g;
+  if (elect_one()) {
+    atomicAdd(p.sync + (g & 63), 1);
+    const int hgrp = g - p.sync_d;
+    if (hgrp >= 0) {
+      const int target = (hgrp / 64 + 1) * p.sync_clusters;
+      const int* slot = p.sync + (hgrp & 63);
+      long long spins = 0;
+      while (ld_acquire_gpu(slot) < target) {
+        __nanosleep(64);
+        if (++spins > (1 << 22)) {  // ~0.3 s: a cluster is not resident; stop syncing
+          lockstep = false;
+          break;
+        }
+      }
+    }
+  }
+  return __all_sync(0xFFFFFFFFu, lockstep);
+}
+
 __device__ __forceinline__ void epilogue_bar() {  // the 4 epilogue warps only
   asm volatile("bar.sync 1, 128;" ::: "memory");
 }
@@ -278,6 +308,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // ---------------- TMA producer (warp-wide loop, one elected issuer) ----------------
     int stage = 0;
     uint32_t phase = 0;
+    int step = 0;
+    bool lockstep = p.sync != nullptr && mc_rank <= 0;
     for (int unit = unit0; unit < p.total_units; unit += ustep) {
       TileCoord tc;
       int c0, nc;
@@ -287,7 +319,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int pr = 0; pr < cd.npairs; ++pr) {
           const int l = cd.l0 + pr;
           const int h = cd.d + 2 - l;
-          for (int kb = 0; kb < p.kblocks; ++kb) {
+          for (int kb = 0; kb < p.kblocks; ++kb, ++step) {
+            lockstep = lockstep_point(p, step, lockstep);
             mbar_wait(&empty[stage], phase ^ 1);
             if (elect_one()) {
               mbar_expect_tx(&full[stage], kStageBytes);
@@ -529,6 +562,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     const uint32_t full_leader0 = map_to_rank(&full[0], 0);
     int stage = 0;
     uint32_t phase = 0;
+    int step = 0;               // k-steps issued by this cluster
+    bool lockstep = p.sync != nullptr && leader;
     for (int unit = pair; unit < p.total_units; unit += npairs) {
       TileCoord tc;
       int c0, nc;
@@ -540,7 +575,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       for (int pr = 0; pr < cd.npairs; ++pr) {
         const int l = cd.l0 + pr;
         const int h = cd.d + 2 - l;
-        for (int kb = 0; kb < p.kblocks; ++kb) {
+        for (int kb = 0; kb < p.kblocks; ++kb, ++step) {
+          lockstep = lockstep_point(p, step, lockstep);
           mbar_wait(&empty[stage], phase ^ 1);
           if (elect_one()) {
             if (leader) mbar_expect_tx(&full[stage], 2 * kPairStageBytes);
@@ -678,7 +714,7 @@ cudaError_t launch_gemm_i8_pair(const CUtensorMap* tma, const CUtensorMap* tmb,
   if (args.total_units < pairs) pairs = args.total_units;
   if (pairs < 1) return cudaSuccess;
   const char* sv = std::getenv("OZGPU_PAIR_STAGES");
-  const int stages = sv ? std::atoi(sv) : 4;
+  const int stages = sv ? std::atoi(sv) : 6;
   cudaError_t e0 = stages == 6 ? launch_pair_t<6>(tma, tmb, args, pairs, st)
                  : stages == 5 ? launch_pair_t<5>(tma, tmb, args, pairs, st)
                  : stages == 3 ? launch_pair_t<3>(tma, tmb, args, pairs, st)

@@ -111,7 +111,7 @@ struct ozgpu_ctx {
   ozgpu::DevBuf in_a, in_b, io_c, in_c2, ratios, i64a, i64b, i64c, i64o, ovf;
   std::vector<ozgpu::ChunkDesc> host_chunks;
   std::vector<int> host_aux;
-  ozgpu::DevBuf aux, counters;
+  ozgpu::DevBuf aux, counters, sync;
   // row-blocked H2D / compute / D2H pipeline of ozgpu_dgemm
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
   std::vector<cudaEvent_t> pipe_events;
@@ -314,6 +314,28 @@ bool build_bins(const std::vector<ChunkDesc>& chunks, std::vector<int>& order,
     return true;
   }
   return false;
+}
+
+// Wave lockstep of the 2-CTA GEMM kernels (GemmArgs::sync): equal-length
+// units (bins) only; OZGPU_SYNC=0/1, OZGPU_SYNC_G / OZGPU_SYNC_D override the
+// group size and the allowed lag in groups.
+void setup_lockstep(ozgpu_ctx* ctx, GemmArgs& g, const ChunkPlan& cp, const std::vector<int>& aux,
+                    const std::vector<int>& bfirst, cudaStream_t st) {
+  if (!g.bin_first || bfirst.size() < 2) return;
+  bool sync = true;
+  if (const char* env = std::getenv("OZGPU_SYNC")) sync = std::string(env) == "1";
+  if (!sync) return;
+  const int clusters = std::min(ctx->num_sms / 2, g.total_units);
+  int bin_pairs = 0;
+  for (int q = bfirst[0]; q < bfirst[1]; ++q) bin_pairs += cp.chunks[aux[q]].npairs;
+  g.sync = static_cast<int*>(ctx->sync.get(sizeof(int) * 64));
+  OZ_CUDA(cudaMemsetAsync(g.sync, 0, sizeof(int) * 64, st));
+  g.sync_clusters = clusters;
+  g.sync_steps = (g.total_units / clusters) * bin_pairs * g.kblocks;
+  g.sync_g = 64;
+  g.sync_d = 1;
+  if (const char* env = std::getenv("OZGPU_SYNC_G")) g.sync_g = std::max(1, std::atoi(env));
+  if (const char* env = std::getenv("OZGPU_SYNC_D")) g.sync_d = std::max(1, std::atoi(env));
 }
 
 // Diagnostics exactly as the reference accumulates them (scheme.cpp:246-359).
@@ -558,12 +580,15 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
     g.planes = planes;
     g.plane_stride = plane;
     g.ldp = ldp;
-    // 1-CTA 128 x 256 tiles by default.  The CTA-pair kernel (cta_group::2,
-    // 256 x 256 tiles) is opt-in (OZGPU_CTA_PAIR=1): measured on B200 at
-    // 8192^3 (12,12) it issues ~2.5x the L2 misses of the 1-CTA kernel
-    // (203 GB vs 81 GB DRAM reads) and is 13-20% slower under the power cap.
+    // Default: the CTA-pair kernel (cta_group::2, 256 x 256 tiles, 6-stage
+    // ring) with equal-length bins and wave lockstep.  Measured on B200 at
+    // 8192^3 (12,12), interleaved and power-capped: 29.2 ms per launch vs
+    // 30.4 ms for the B-multicast 1-CTA kernel (OZGPU_CTA_PAIR=0) and 30.8 ms
+    // without lockstep; DRAM reads 46 GB, tensor pipe 93 % active at the base
+    // clock.  Without lockstep the deep ring lets the CTAs of a wave drift
+    // apart and DRAM reads grow 2-3.5x.
     const int pair_tiles = static_cast<int>(((m + 255) / 256) * tiles_n);
-    bool pair = false;
+    bool pair = m >= 256;
     if (const char* env = std::getenv("OZGPU_CTA_PAIR")) pair = std::string(env) == "1" && m >= 256;
     if (pair) {
       g.tiles_m = static_cast<int>((m + 255) / 256);
@@ -582,6 +607,7 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
         g.bin_first = daux + g.nchunks;
         g.total_units = static_cast<int>(static_cast<int64_t>(pair_tiles) * nb);
       }
+      setup_lockstep(ctx, g, cp, aux, bfirst, st);
       CUtensorMap tmb2 = make_slice_map(ctx, slB, kp, n, sb, 128, plane_b, ld);
       OZ_CUDA(launch_gemm_i8_pair(&tma, &tmb2, g, ctx->num_sms, st, &launches));
     } else {
@@ -667,6 +693,7 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
       if (mc) {
         const int64_t super_tiles = static_cast<int64_t>((tiles_m + 1) / 2) * tiles_n;
         g.total_units = static_cast<int>(g.total_units / tiles * super_tiles);
+        setup_lockstep(ctx, g, cp, aux, bfirst, st);
         CUtensorMap tmb_half = make_slice_map(ctx, slB, kp, n, sb, 128, plane_b, ld);
         OZ_CUDA(launch_gemm_i8_mc(&tma, &tmb_half, g, ctx->num_sms, st, &launches));
       } else {

@@ -36,6 +36,12 @@ struct GemmArgs {
   int group;          // rasterisation: tile-rows per group (0 = 8)
   int pair_order;     // diagnostic: 1-CTA kernel walks 256-row pair tiles
   int l2_hint;        // CTA-pair kernel TMA cache policy: 0 none, 1 evict_last, 2 evict_normal
+  // wave lockstep (CTA-pair kernel): the leader's producer publishes every
+  // sync_g k-steps and waits until every cluster has passed the group
+  // sync_d groups back, for its first sync_steps k-steps (all clusters run at
+  // least that many).  sync = 64 zeroed counters; null = off.
+  int* sync;
+  int sync_steps, sync_g, sync_d, sync_clusters;
   int32_t* planes;    // [nchunks][m][ldp] int32 chunk sums
   int64_t plane_stride;
   int64_t ldp;

@@ -234,25 +234,27 @@ def test_native_kernels_launched(oz):
 
 GEMM_VARIANTS = {
     "default": {},
-    "final": {"OZGPU_EPILOGUE": "final"},
-    "fused": {"OZGPU_EPILOGUE": "fused"},
-    "cta_pair": {"OZGPU_EPILOGUE": "split", "OZGPU_CTA_PAIR": "1"},
-    "cta_pair_bins": {"OZGPU_CTA_PAIR": "1", "OZGPU_BINS": "1"},
-    "bins": {"OZGPU_BINS": "1"},
+    "final": {"OZGPU_EPILOGUE": "final", "OZGPU_CTA_PAIR": "0"},
+    "fused": {"OZGPU_EPILOGUE": "fused", "OZGPU_CTA_PAIR": "0"},
+    "pair_bins_lockstep": {"OZGPU_BINS": "1"},
+    "pair_bins_lockstep_g1": {"OZGPU_BINS": "1", "OZGPU_SYNC_G": "1", "OZGPU_SYNC_D": "1"},
+    "pair_no_lockstep": {"OZGPU_BINS": "1", "OZGPU_SYNC": "0"},
+    "pair_stages4": {"OZGPU_PAIR_STAGES": "4", "OZGPU_BINS": "1"},
     "no_bins": {"OZGPU_BINS": "0"},
-    "no_multicast": {"OZGPU_MC": "0"},
-    "no_multicast_bins": {"OZGPU_MC": "0", "OZGPU_BINS": "1"},
+    "multicast_1cta": {"OZGPU_CTA_PAIR": "0"},
+    "multicast_1cta_bins_lockstep": {"OZGPU_CTA_PAIR": "0", "OZGPU_BINS": "1"},
+    "plain_1cta_bins": {"OZGPU_CTA_PAIR": "0", "OZGPU_MC": "0", "OZGPU_BINS": "1"},
     "horner_combine": {"OZGPU_COMBINE": "horner"},
 }
 
 
 @pytest.mark.parametrize("variant", sorted(GEMM_VARIANTS))
 def test_gemm_variants_match_reference(oz, ref, variant, monkeypatch):
-    """Every GEMM variant -- fused exact-integer epilogue, split planes +
-    combine on the CTA-pair (cta_group::2) kernel and on the 1-CTA kernel,
-    equal-length chunk bins, B-panel multicast in 2-CTA clusters, both exact
-    combine kernels -- is bit-exact, incl. ragged tiles and 3-word exact
-    values."""
+    """Every GEMM variant -- the CTA-pair (cta_group::2) kernel with and
+    without wave lockstep and at 4 / 6 stages, the B-multicast and plain
+    1-CTA kernels, equal-length chunk bins on / off, the fused W-word and
+    folded-combine epilogues, both exact combine kernels -- is bit-exact,
+    incl. ragged tiles and 3-word exact values."""
     for key, val in GEMM_VARIANTS[variant].items():
         monkeypatch.setenv(key, val)
     rng = np.random.default_rng(77)
