@@ -152,11 +152,11 @@ __device__ __forceinline__ bool lockstep_point(const GemmArgs& p, int step, bool
   if (step >= p.sync_steps) return false;
   const int g = step / p.sync_g;
   if (elect_one()) {
-    atomicAdd(p.sync + (g & 63), 1);
+    atomicAdd(p.sync + (g & 63) * 32, 1);  // one 128-byte line per slot
     const int hgrp = g - p.sync_d;
     if (hgrp >= 0) {
       const int target = (hgrp / 64 + 1) * p.sync_clusters;
-      const int* slot = p.sync + (hgrp & 63);
+      const int* slot = p.sync + (hgrp & 63) * 32;
       long long spins = 0;
       while (ld_acquire_gpu(slot) < target) {
         __nanosleep(64);

@@ -328,8 +328,8 @@ void setup_lockstep(ozgpu_ctx* ctx, GemmArgs& g, const ChunkPlan& cp, const std:
   const int clusters = std::min(ctx->num_sms / 2, g.total_units);
   int bin_pairs = 0;
   for (int q = bfirst[0]; q < bfirst[1]; ++q) bin_pairs += cp.chunks[aux[q]].npairs;
-  g.sync = static_cast<int*>(ctx->sync.get(sizeof(int) * 64));
-  OZ_CUDA(cudaMemsetAsync(g.sync, 0, sizeof(int) * 64, st));
+  g.sync = static_cast<int*>(ctx->sync.get(sizeof(int) * 64 * 32));
+  OZ_CUDA(cudaMemsetAsync(g.sync, 0, sizeof(int) * 64 * 32, st));
   g.sync_clusters = clusters;
   g.sync_steps = (g.total_units / clusters) * bin_pairs * g.kblocks;
   g.sync_g = 64;

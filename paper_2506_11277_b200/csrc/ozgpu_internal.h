@@ -39,7 +39,7 @@ struct GemmArgs {
   // wave lockstep (CTA-pair kernel): the leader's producer publishes every
   // sync_g k-steps and waits until every cluster has passed the group
   // sync_d groups back, for its first sync_steps k-steps (all clusters run at
-  // least that many).  sync = 64 zeroed counters; null = off.
+  // least that many).  sync = 64 zeroed counters, 128 bytes apart; null = off.
   int* sync;
   int sync_steps, sync_g, sync_d, sync_clusters;
   int32_t* planes;    // [nchunks][m][ldp] int32 chunk sums
