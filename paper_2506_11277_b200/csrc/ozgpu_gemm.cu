@@ -160,7 +160,7 @@ __device__ __forceinline__ bool lockstep_point(const GemmArgs& p, int step, bool
       long long spins = 0;
       while (ld_acquire_gpu(slot) < target) {
         __nanosleep(64);
-        if (++spins > (1 << 22)) {  // ~0.3 s: a cluster is not resident; stop syncing
+        if (++spins > (1 << 16)) {  // ~50 ms: a cluster is not resident; stop syncing
           lockstep = false;
           break;
         }
