@@ -7,7 +7,10 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <unistd.h>
+
 #include <algorithm>
+#include <map>
 #include <array>
 #include <atomic>
 #include <cmath>
@@ -65,12 +68,17 @@ int guarded(F&& f) {
   }
 }
 
+// Bumped whenever a workspace buffer is (re)allocated: captured CUDA graphs
+// hold raw workspace pointers and are re-captured when it changes.
+std::atomic<uint64_t> g_workspace_gen{0};
+
 // A grow-only device allocation.
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
   void* get(size_t want) {
     if (want > bytes) {
+      g_workspace_gen.fetch_add(1);
       if (p) cudaFree(p);
       p = nullptr;
       bytes = 0;
@@ -111,6 +119,18 @@ struct ozgpu_ctx {
   ozgpu::DevBuf in_a, in_b, io_c, in_c2, ratios, i64a, i64b, i64c, i64o, ovf;
   std::vector<ozgpu::ChunkDesc> host_chunks;
   std::vector<int> host_aux;
+  // CUDA-graph replay of ozgpu_dgemm_device (same shape, plan, pointers and
+  // stream -> one cudaGraphLaunch): host-side tables uploaded by a captured
+  // graph are staged in pinned buffers owned by the graph entry
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    uint64_t gen = 0;
+    int64_t launches = 0;
+    int uses = 0;
+    std::vector<void*> pinned;
+  };
+  std::map<std::string, GraphEntry> graphs;
+  GraphEntry* capturing = nullptr;
   ozgpu::DevBuf aux, counters, sync;
   // row-blocked H2D / compute / D2H pipeline of ozgpu_dgemm
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
@@ -425,6 +445,20 @@ int exact_words(int diagonals, int width, size_t nchunks) {
   throw std::invalid_argument("multiply: exact accumulator wider than 1024 bits");
 }
 
+// Host -> device copy of a small host-built table on `st`.  Inside a graph
+// capture the source is first staged in pinned memory owned by the graph, so
+// the captured copy node stays valid for every replay.
+void upload_table(ozgpu_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (ctx->capturing) {
+    void* pin = nullptr;
+    OZ_CUDA(cudaMallocHost(&pin, bytes));
+    std::memcpy(pin, src, bytes);
+    ctx->capturing->pinned.push_back(pin);
+    src = pin;
+  }
+  OZ_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+}
+
 // Operands already sliced by the caller (the blocked pipeline of
 // host_multiply): a row range of the [count][rows][kp] slice buffers, with
 // the full buffers' plane stride, and the matching scales.
@@ -526,8 +560,7 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
     }
     ChunkDesc* dchunks =
         static_cast<ChunkDesc*>(ctx->chunks.get(sizeof(ChunkDesc) * cp.chunks.size()));
-    OZ_CUDA(cudaMemcpyAsync(dchunks, cp.chunks.data(), sizeof(ChunkDesc) * cp.chunks.size(),
-                            cudaMemcpyHostToDevice, st));
+    upload_table(ctx, dchunks, cp.chunks.data(), sizeof(ChunkDesc) * cp.chunks.size(), st);
     ctx->host_chunks = cp.chunks;
 
     CUtensorMap tma = make_slice_map(ctx, slA, kp, m, sa, kBlockM, plane_a, ld);
@@ -601,8 +634,7 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
         const size_t nb = bfirst.size() - 1;
         aux.insert(aux.end(), bfirst.begin(), bfirst.end());
         int* daux = static_cast<int*>(ctx->aux.get(sizeof(int) * aux.size()));
-        OZ_CUDA(cudaMemcpyAsync(daux, aux.data(), sizeof(int) * aux.size(),
-                                cudaMemcpyHostToDevice, st));
+        upload_table(ctx, daux, aux.data(), sizeof(int) * aux.size(), st);
         g.proc_order = daux;
         g.bin_first = daux + g.nchunks;
         g.total_units = static_cast<int>(static_cast<int64_t>(pair_tiles) * nb);
@@ -637,8 +669,7 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
           aux.push_back(d == cp.diagonals ? g.nchunks : cc);
         }
         int* daux = static_cast<int*>(ctx->aux.get(sizeof(int) * aux.size()));
-        OZ_CUDA(cudaMemcpyAsync(daux, aux.data(), sizeof(int) * aux.size(),
-                                cudaMemcpyHostToDevice, st));
+        upload_table(ctx, daux, aux.data(), sizeof(int) * aux.size(), st);
         int* counters = static_cast<int*>(ctx->counters.get(sizeof(int) * tiles));
         OZ_CUDA(cudaMemsetAsync(counters, 0, sizeof(int) * tiles, st));
         g.proc_order = daux;
@@ -677,8 +708,7 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
         const size_t nb = bfirst.size() - 1;
         aux.insert(aux.end(), bfirst.begin(), bfirst.end());
         int* daux = static_cast<int*>(ctx->aux.get(sizeof(int) * aux.size()));
-        OZ_CUDA(cudaMemcpyAsync(daux, aux.data(), sizeof(int) * aux.size(),
-                                cudaMemcpyHostToDevice, st));
+        upload_table(ctx, daux, aux.data(), sizeof(int) * aux.size(), st);
         g.proc_order = daux;
         g.bin_first = daux + g.nchunks;
         g.total_units = static_cast<int>(tiles * static_cast<int64_t>(nb));
@@ -1076,6 +1106,10 @@ int ozgpu_destroy(ozgpu_ctx* ctx) {
     for (cudaEvent_t e : ctx->pipe_events) cudaEventDestroy(e);
     for (auto& ev : ctx->pending_events)
       for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    for (auto& kv : ctx->graphs) {
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+      for (void* pp : kv.second.pinned) cudaFreeHost(pp);
+    }
     for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
     delete ctx;
   });
@@ -1327,6 +1361,73 @@ int ozgpu_dgemm_device(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const do
     std::lock_guard<std::mutex> lock(ctx->mu);
     OZ_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t st = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
+    // Repeated calls with the same shape, plan, pointers and stream replay a
+    // captured CUDA graph (one launch instead of ~10 enqueues and the host
+    // planning); the first call runs eagerly (it also sizes the workspace),
+    // the second captures.  Off with OZGPU_GRAPH=0, under stage timing, on
+    // the legacy default stream, and for the sequential strategies.
+    const char* genv = std::getenv("OZGPU_GRAPH");
+    const bool graphs = !(genv && std::string(genv) == "0") && !ctx->timing && st != nullptr &&
+                        plan->strategy == 2;
+    if (graphs) {
+      char key[512];
+      std::snprintf(key, sizeof key, "%p|%lld|%lld|%lld|%p|%lld|%p|%lld|%p|%lld|%p|%d|%d|%d|%d|%d|%d|%d|%d|%d|%d",
+                    stream, (long long)m, (long long)n, (long long)k, (const void*)a, (long long)lda,
+                    (const void*)b, (long long)ldb, (void*)c, (long long)ldc, (void*)dev_status,
+                    cfg.input_width, cfg.acc_width, plan->slices_a, plan->slices_b, plan->width,
+                    plan->schedule, plan->strategy, plan->mode, plan->precision,
+                    plan->diag_sum_limit);
+      // the OZGPU_* knobs select kernels at capture time: part of the key
+      std::string gkey(key);
+      for (char** ev = environ; ev && *ev; ++ev)
+        if (std::strncmp(*ev, "OZGPU_", 6) == 0) gkey += std::string("|") + *ev;
+      auto& e = ctx->graphs[gkey];
+      const uint64_t gen = g_workspace_gen.load();
+      if (e.exec && e.gen == gen) {
+        OZ_CUDA(cudaGraphLaunch(e.exec, st));
+        ctx->launches += e.launches;
+        if (diag) *diag = make_diag(*plan, cfg, m, n, k, 0);
+        return;
+      }
+      if (e.exec) {  // stale: the workspace moved
+        cudaGraphExecDestroy(e.exec);
+        e.exec = nullptr;
+        for (void* pp : e.pinned) cudaFreeHost(pp);
+        e.pinned.clear();
+      }
+      if (e.uses++ >= 1) {
+        cudaGraph_t graph = nullptr;
+        const int64_t before = ctx->launches.load();
+        ctx->capturing = &e;
+        OZ_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+        try {
+          run_multiply(ctx, m, n, k, a, lda, b, ldb, c, ldc, cfg, *plan, st, dev_status, false,
+                       1.0, 0.0, nullptr, 0);
+        } catch (...) {
+          ctx->capturing = nullptr;
+          cudaStreamEndCapture(st, &graph);
+          if (graph) cudaGraphDestroy(graph);
+          throw;
+        }
+        ctx->capturing = nullptr;
+        OZ_CUDA(cudaStreamEndCapture(st, &graph));
+        e.launches = ctx->launches.load() - before;
+        ctx->launches -= e.launches;  // counted when replayed
+        OZ_CUDA(cudaGraphInstantiate(&e.exec, graph, 0));
+        cudaGraphDestroy(graph);
+        e.gen = g_workspace_gen.load();
+        if (e.gen != gen) {  // the capture itself grew the workspace: do not trust it
+          cudaGraphExecDestroy(e.exec);
+          e.exec = nullptr;
+          e.uses = 1;
+        } else {
+          OZ_CUDA(cudaGraphLaunch(e.exec, st));
+          ctx->launches += e.launches;
+          if (diag) *diag = make_diag(*plan, cfg, m, n, k, 0);
+          return;
+        }
+      }
+    }
     run_multiply(ctx, m, n, k, a, lda, b, ldb, c, ldc, cfg, *plan, st, dev_status, false, 1.0,
                  0.0, nullptr, 0);
     if (diag) *diag = make_diag(*plan, cfg, m, n, k, 0);
