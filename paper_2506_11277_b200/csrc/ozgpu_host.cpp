@@ -134,6 +134,9 @@ struct ozgpu_ctx {
   ozgpu::DevBuf aux, counters, sync;
   // row-blocked H2D / compute / D2H pipeline of ozgpu_dgemm
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  // B's slicing runs on a forked stream, joined before the GEMM
+  cudaStream_t fork_stream = nullptr;
+  cudaEvent_t fork_ev[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> pipe_events;
   // stage timing (ozgpu_set_stage_timing)
   bool timing = false;
@@ -516,10 +519,30 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
     auto* colmax = static_cast<unsigned long long*>(ctx->colmax.get(8 * (n + 1)));
     int* status = dev_status ? dev_status : static_cast<int*>(ctx->status.get(sizeof(int)));
     OZ_CUDA(cudaMemsetAsync(status, 0, sizeof(int), st));
+    // A's and B's slicing are independent: B's runs on a forked stream so
+    // the two HBM-bound chains overlap (their tails and the short memsets
+    // hide each other); joined before the GEMM.  OZGPU_SLICE_FORK=0: serial.
+    const char* fv = std::getenv("OZGPU_SLICE_FORK");
+    const bool fork = !(fv && std::string(fv) == "0") && m > 0 && n > 0;
+    cudaStream_t sb_st = st;
+    if (fork) {
+      if (!ctx->fork_stream) {
+        OZ_CUDA(cudaStreamCreateWithFlags(&ctx->fork_stream, cudaStreamNonBlocking));
+        OZ_CUDA(cudaEventCreateWithFlags(&ctx->fork_ev[0], cudaEventDisableTiming));
+        OZ_CUDA(cudaEventCreateWithFlags(&ctx->fork_ev[1], cudaEventDisableTiming));
+      }
+      OZ_CUDA(cudaEventRecord(ctx->fork_ev[0], st));
+      OZ_CUDA(cudaStreamWaitEvent(ctx->fork_stream, ctx->fork_ev[0], 0));
+      sb_st = ctx->fork_stream;
+    }
+    OZ_CUDA(launch_slice_cols(db, ldb, k, n, ld, t, sb, p.mode, wb, 0, wqb, colmax, status, sb_st,
+                              &launches));
     OZ_CUDA(launch_slice_rows(da, lda, m, k, ld, t, sa, p.mode, wa, 0, wqa, status, st,
                               &launches));
-    OZ_CUDA(launch_slice_cols(db, ldb, k, n, ld, t, sb, p.mode, wb, 0, wqb, colmax, status, st,
-                              &launches));
+    if (fork) {
+      OZ_CUDA(cudaEventRecord(ctx->fork_ev[1], sb_st));
+      OZ_CUDA(cudaStreamWaitEvent(st, ctx->fork_ev[1], 0));
+    }
     slA = wa;
     slB = wb;
     qa = wqa;
@@ -1104,6 +1127,12 @@ int ozgpu_destroy(ozgpu_ctx* ctx) {
       cudaStreamDestroy(ctx->d2h_stream);
     }
     for (cudaEvent_t e : ctx->pipe_events) cudaEventDestroy(e);
+    if (ctx->fork_stream) {
+      cudaStreamSynchronize(ctx->fork_stream);
+      cudaStreamDestroy(ctx->fork_stream);
+      cudaEventDestroy(ctx->fork_ev[0]);
+      cudaEventDestroy(ctx->fork_ev[1]);
+    }
     for (auto& ev : ctx->pending_events)
       for (cudaEvent_t e : ev) cudaEventDestroy(e);
     for (auto& kv : ctx->graphs) {
