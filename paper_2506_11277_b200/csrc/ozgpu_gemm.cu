@@ -693,15 +693,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   }
 }
 
+// cudaFuncSetAttribute is per device: remember which devices a kernel's
+// dynamic shared-memory limit was raised on (bit per device ordinal).
+__host__ inline bool needs_config(unsigned long long& done_mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ULL << (dev & 63);
+  if (done_mask & bit) return false;
+  done_mask |= bit;
+  return true;
+}
+
 template <int S>
 static cudaError_t launch_pair_t(const CUtensorMap* tma, const CUtensorMap* tmb,
                                  const GemmArgs& args, int pairs, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
+  static unsigned long long configured = 0;
+  if (needs_config(configured)) {
     cudaError_t e = cudaFuncSetAttribute(gemm_i8_pair_kernel<S>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pair(S));
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   gemm_i8_pair_kernel<S><<<2 * pairs, kGemmThreads, smem_pair(S), st>>>(*tma, *tmb, args);
   return cudaSuccess;
@@ -728,12 +738,11 @@ cudaError_t launch_gemm_i8_pair(const CUtensorMap* tma, const CUtensorMap* tmb,
 template <int W>
 static cudaError_t launch_t(const CUtensorMap* tma, const CUtensorMap* tmb, const GemmArgs& args,
                             int grid, int smem, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
+  static unsigned long long configured = 0;
+  if (needs_config(configured)) {
     cudaError_t e = cudaFuncSetAttribute(gemm_i8_kernel<W, false, 4>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   gemm_i8_kernel<W, false, 4><<<grid, kGemmThreads, smem, st>>>(*tma, *tmb, args);
   return cudaGetLastError();
@@ -743,12 +752,11 @@ template <int S>
 static cudaError_t launch_mc_t(const CUtensorMap* tma, const CUtensorMap* tmb_half,
                                const GemmArgs& args, int clusters, cudaStream_t st) {
   constexpr int smem = S * kStageBytes + 1024 + 256;
-  static bool configured = false;
-  if (!configured) {
+  static unsigned long long configured = 0;
+  if (needs_config(configured)) {
     cudaError_t e = cudaFuncSetAttribute(gemm_i8_kernel<0, true, S>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * clusters);
