@@ -225,16 +225,12 @@ __device__ __forceinline__ void emit8_trunc_i8(const double (&v)[8], int q, int 
       const int l = j * SPW + i;
       if (l >= count) break;
       const int s = WB - T * (i + 1);
-      // one funnel shift per entry brings the slice to byte 0; three byte
-      // permutes pack 4 entries' bytes, one AND masks them to T bits
-      uint32_t u[8];
+      uint32_t lo = 0, hi = 0;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) u[e] = static_cast<uint32_t>(w[e] >> s);
-      const uint32_t mask4 = TMASK * 0x01010101u;
-      uint32_t lo = __byte_perm(__byte_perm(u[0], u[1], 0x0040), __byte_perm(u[2], u[3], 0x0040),
-                                0x5410) & mask4;
-      uint32_t hi = __byte_perm(__byte_perm(u[4], u[5], 0x0040), __byte_perm(u[6], u[7], 0x0040),
-                                0x5410) & mask4;
+      for (int e = 0; e < 4; ++e) {
+        lo |= (static_cast<uint32_t>(w[e] >> s) & TMASK) << (8 * e);
+        hi |= (static_cast<uint32_t>(w[e + 4] >> s) & TMASK) << (8 * e);
+      }
       lo = __vsub4(lo ^ neg_lo, neg_lo);
       hi = __vsub4(hi ^ neg_hi, neg_hi);
       *reinterpret_cast<uint2*>(out + l * plane + off) = make_uint2(lo, hi);
