@@ -50,8 +50,8 @@ CONFIGS = {
                     "estimator-chosen slices for 1e-15",
                m=65536, n=2048, k=2048, gen="uniform", slices="estimator"),
     "c5": dict(name="configs[4]: FP64 GEMM m=n=k=32768, uniform(-0.5,0.5), estimator-chosen "
-                    "slices for 1e-15",
-               m=32768, n=32768, k=32768, gen="uniform", slices="estimator"),
+                    "slices for 1e-15, 2-D C tiles over the ranks (strong scaling)",
+               m=32768, n=32768, k=32768, gen="uniform", slices="estimator", strong=True),
     "ns": dict(name="north star: FP64 GEMM m=n=k=16384, uniform(-0.5,0.5), estimator-chosen "
                     "slices for 1e-15",
                m=16384, n=16384, k=16384, gen="uniform", slices="estimator"),
@@ -289,7 +289,17 @@ def main():
     cfg = dict(CONFIGS[args.config])
     m, n, k = cfg["m"], cfg["n"], cfg["k"]
     pr, pc = shard.grid_for(world)
-    blk = shard.block_of(rank, world, pr * m, pc * n)
+    strong = bool(cfg.get("strong"))
+    if strong:
+        # a fixed global m x n split into the ranks' C blocks
+        blk = shard.block_of(rank, world, m, n)
+        gm, gn = m, n
+        m, n = blk.row1 - blk.row0, blk.col1 - blk.col0
+        cfg["m"], cfg["n"] = m, n
+    else:
+        # weak scaling: every rank a full m x n block of a (p_r m) x (p_c n) product
+        blk = shard.block_of(rank, world, pr * m, pc * n)
+        gm, gn = pr * m, pc * n
     mcfg = oz.MmaConfig.int8_int32()
     dev = torch.device(f"cuda:{local}")
     # a dedicated stream: CUDA events and the library's kernels share it
@@ -364,8 +374,9 @@ def main():
     oz.set_stage_timing(False)
     slice_ms, gemm_ms, comb_ms, calls = oz.stage_times(reset=True)
 
-    flops_rank = 2.0 * m * n * k
-    value = flops_rank * world / (ms * 1e-3) / 1e12
+    flops_rank = 2.0 * m * n * k  # this rank's block
+    flops_total = 2.0 * gm * gn * k  # the whole job (all ranks' blocks)
+    value = flops_total / (ms * 1e-3) / 1e12
     gemm_ms_call = gemm_ms / max(calls, 1)
     int8_ops = 2.0 * chi * m * n * k
     tops = int8_ops / (gemm_ms_call * 1e-3) / 1e12
@@ -385,12 +396,13 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
+        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
+        "dtype": "int8",
         "data": "synthetic: reference generator random_uniform(-0.5,0.5) seeds 1,2 "
                 "(per-panel seeds 1+1000i / 2+1000j for N>1)" if cfg["gen"] == "uniform" else
                 "synthetic: reference gen_kappa_d(2^60, seed 7, rotate)",
         "config": {"workload": cfg["name"], "m": m, "n": n, "k": k,
-                   "global_m": pr * m, "global_n": pc * n, "grid": [pr, pc],
+                   "global_m": gm, "global_n": gn, "grid": [pr, pc],
                    "slices": list(slices), "chi": chi, "width": plan.width,
                    "schedule": "reduced", "strategy": "levelled-exact", "estimator": est,
                    "launch": "CUDA-graph replay of the whole multiply (captured on the 2nd call); "
@@ -433,7 +445,7 @@ def main():
             oz.set_stage_timing(False)
             _, g_ms, _, c_ = oz.stage_times(reset=True)
             ch = oz.chi(s, s)
-            sweep.append({"s": s, "chi": ch, "tflops": flops_rank * world / (sms * 1e-3) / 1e12,
+            sweep.append({"s": s, "chi": ch, "tflops": flops_total / (sms * 1e-3) / 1e12,
                           "int8_tops": 2.0 * ch * m * n * k / (g_ms / max(c_, 1) * 1e-3) / 1e12,
                           "ms_per_step": sms})
         line["sweep"] = sweep
@@ -455,7 +467,7 @@ def main():
             t = torch.tensor([el], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
-        line["e2e"] = {"value": flops_rank * world / el / 1e12, "unit": "TFLOP/s",
+        line["e2e"] = {"value": flops_total / el / 1e12, "unit": "TFLOP/s",
                        "h2d_bytes_per_step": 8 * (m * k + k * n), "d2h_bytes_per_step": 8 * m * n,
                        "ms_per_step": el * 1e3, "api": "ozgpu_dgemm (host pointers, pinned)"}
 

@@ -550,6 +550,44 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
   }
   if (ctx->timing) OZ_CUDA(cudaEventRecord(ev[1], st));
 
+  // Chunk-plane memory budget: the int32 planes cost 4 * chunks * m * n
+  // bytes (72 GiB for 32768^3 at (13,12)); beyond the budget the GEMM +
+  // combine run over row blocks of C against the slices already in HBM
+  // (blocking is exact: scales are per row of A / column of B).
+  if (p.strategy == 2 && m > 512 && n > 0 && !cp.chunks.empty()) {
+    const int64_t ldp_b = round_up(n, 4);
+    const double plane_bytes = 4.0 * static_cast<double>(cp.chunks.size()) * m * ldp_b;
+    double budget = 0.0;
+    if (const char* env = std::getenv("OZGPU_PLANE_BUDGET_GB")) {
+      budget = std::atof(env) * 1073741824.0;
+    } else {
+      size_t free_b = 0, total_b = 0;
+      OZ_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      budget = 0.25 * static_cast<double>(total_b);
+    }
+    if (plane_bytes > budget) {
+      const double per_row = 4.0 * static_cast<double>(cp.chunks.size()) * ldp_b;
+      int64_t rows = static_cast<int64_t>(budget / per_row) / 256 * 256;
+      rows = std::max<int64_t>(rows, 256);
+      const bool timing = ctx->timing;
+      ctx->timing = false;  // the blocks' GEMM + combine are timed as one stage
+      for (int64_t r0 = 0; r0 < m; r0 += rows) {
+        const int64_t r1 = std::min(m, r0 + rows);
+        Presliced sub{slA + r0 * ld, plane_a, qa + r0, slB, plane_b, qb, ld};
+        run_multiply(ctx, r1 - r0, n, k, nullptr, 0, nullptr, 0, dc + r0 * ldc, ldc, cfg, p, st,
+                     nullptr, axpby, alpha, beta, dcin ? dcin + r0 * ldcin : nullptr, ldcin, &sub);
+      }
+      ctx->timing = timing;
+      if (ctx->timing) {
+        OZ_CUDA(cudaEventRecord(ev[2], st));
+        OZ_CUDA(cudaEventRecord(ev[3], st));
+        ctx->pending_events.push_back(ev);
+      }
+      ctx->launches += launches;
+      return nullptr;
+    }
+  }
+
   int* psi_dev = nullptr;
   if (m > 0 && n > 0 && !cp.chunks.empty()) {
     const int tiles_m = static_cast<int>((m + kBlockM - 1) / kBlockM);

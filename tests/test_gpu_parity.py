@@ -245,6 +245,7 @@ GEMM_VARIANTS = {
     "multicast_1cta_bins_lockstep": {"OZGPU_CTA_PAIR": "0", "OZGPU_BINS": "1"},
     "plain_1cta_bins": {"OZGPU_CTA_PAIR": "0", "OZGPU_MC": "0", "OZGPU_BINS": "1"},
     "horner_combine": {"OZGPU_COMBINE": "horner"},
+    "plane_budget_row_blocks": {"OZGPU_PLANE_BUDGET_GB": "0.002"},
 }
 
 
