@@ -297,8 +297,8 @@ ChunkPlan build_chunks(const ozgpu_plan& p, const ozgpu_mma_config& cfg, int64_t
 // same length and the CTAs of a wave stay in step (they then stream the same
 // slice pair at the same time and share it through L2).  Tries bin sizes
 // from the largest chunk upward and keeps the first packing in which every
-// bin is full; returns false (no bins) if none is.  For the reduced schedule
-// the diagonals 1..L pair up as (1, L), (2, L-1), ... into bins of L + 1.
+// bin is full, then consecutive cuts (below).  For the reduced schedule the
+// diagonals 1..L pair up as (1, L), (2, L-1), ... into bins of L + 1.
 bool build_bins(const std::vector<ChunkDesc>& chunks, std::vector<int>& order,
                 std::vector<int>& first) {
   const int nc = static_cast<int>(chunks.size());
@@ -334,6 +334,31 @@ bool build_bins(const std::vector<ChunkDesc>& chunks, std::vector<int>& order,
       order.insert(order.end(), b.begin(), b.end());
     }
     first.push_back(static_cast<int>(order.size()));
+    return true;
+  }
+  // No first-fit packing (e.g. k = 32768: int32 capacity 4 pairs per chunk,
+  // lengths 1..4): cut the chunks in diagonal order into consecutive runs of
+  // equal length -- the smallest length that divides the pair count and
+  // falls on chunk boundaries; at worst one bin holds every chunk (a unit is
+  // then a whole tile, still equal-length).
+  for (int len = maxlen; len <= total; ++len) {
+    if (total % len) continue;
+    std::vector<int> cut{0};
+    int acc = 0;
+    bool ok = true;
+    for (int c = 0; c < nc && ok; ++c) {
+      acc += chunks[c].npairs;
+      if (acc == len) {
+        cut.push_back(c + 1);
+        acc = 0;
+      } else if (acc > len) {
+        ok = false;
+      }
+    }
+    if (!ok || acc != 0) continue;
+    order.resize(nc);
+    for (int c = 0; c < nc; ++c) order[c] = c;
+    first = cut;
     return true;
   }
   return false;
