@@ -147,8 +147,25 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* ptr) {
 // would otherwise keep them together -- measured on B200, the drift doubles
 // or triples DRAM reads.  Every sync_g k-steps the cluster publishes its
 // group and waits until all clusters have passed the group sync_d back.
-__device__ __forceinline__ bool lockstep_point(const GemmArgs& p, int step, bool lockstep) {
-  if (!lockstep || step % p.sync_g != 0) return lockstep;
+__device__ __forceinline__ int ld_relaxed_gpu(const int* ptr) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
+  return v;
+}
+// `seen` carries a prefetched read of the next wait slot: it is issued half
+// a group early so that, in the common case, the check at the boundary costs
+// no round trip and the producer keeps its ring full.
+__device__ __forceinline__ bool lockstep_point(const GemmArgs& p, int step, bool lockstep,
+                                               int& seen) {
+  if (!lockstep) return false;
+  const int r = step % p.sync_g;
+  if (p.sync_prefetch && r == p.sync_g / 2 && r != 0) {  // prefetch the next boundary's slot
+    const int hgrp = step / p.sync_g + 1 - p.sync_d;
+    if (hgrp >= 0 && elect_one()) seen = ld_relaxed_gpu(p.sync + (hgrp & 63) * 32);
+    __syncwarp();
+    return true;
+  }
+  if (r != 0) return true;
   if (step >= p.sync_steps) return false;
   const int g = step / p.sync_g;
   if (elect_one()) {
@@ -157,15 +174,18 @@ __device__ __forceinline__ bool lockstep_point(const GemmArgs& p, int step, bool
     if (hgrp >= 0) {
       const int target = (hgrp / 64 + 1) * p.sync_clusters;
       const int* slot = p.sync + (hgrp & 63) * 32;
-      long long spins = 0;
-      while (ld_acquire_gpu(slot) < target) {
-        __nanosleep(64);
-        if (++spins > (1 << 16)) {  // ~50 ms: a cluster is not resident; stop syncing
-          lockstep = false;
-          break;
+      if (seen < target) {
+        long long spins = 0;
+        while (ld_acquire_gpu(slot) < target) {
+          __nanosleep(64);
+          if (++spins > (1 << 16)) {  // ~50 ms: a cluster is not resident; stop syncing
+            lockstep = false;
+            break;
+          }
         }
       }
     }
+    seen = -1;
   }
   return __all_sync(0xFFFFFFFFu, lockstep);
 }
@@ -310,6 +330,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint32_t phase = 0;
     int step = 0;
     bool lockstep = p.sync != nullptr && mc_rank <= 0;
+    int seen = -1;
     for (int unit = unit0; unit < p.total_units; unit += ustep) {
       TileCoord tc;
       int c0, nc;
@@ -320,7 +341,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const int l = cd.l0 + pr;
           const int h = cd.d + 2 - l;
           for (int kb = 0; kb < p.kblocks; ++kb, ++step) {
-            lockstep = lockstep_point(p, step, lockstep);
+            lockstep = lockstep_point(p, step, lockstep, seen);
             mbar_wait(&empty[stage], phase ^ 1);
             if (elect_one()) {
               mbar_expect_tx(&full[stage], kStageBytes);
@@ -564,6 +585,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     uint32_t phase = 0;
     int step = 0;               // k-steps issued by this cluster
     bool lockstep = p.sync != nullptr && leader;
+    int seen = -1;
     for (int unit = pair; unit < p.total_units; unit += npairs) {
       TileCoord tc;
       int c0, nc;
@@ -576,7 +598,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         const int l = cd.l0 + pr;
         const int h = cd.d + 2 - l;
         for (int kb = 0; kb < p.kblocks; ++kb, ++step) {
-          lockstep = lockstep_point(p, step, lockstep);
+          lockstep = lockstep_point(p, step, lockstep, seen);
           mbar_wait(&empty[stage], phase ^ 1);
           if (elect_one()) {
             if (leader) mbar_expect_tx(&full[stage], 2 * kPairStageBytes);

@@ -384,6 +384,8 @@ void setup_lockstep(ozgpu_ctx* ctx, GemmArgs& g, const ChunkPlan& cp, const std:
   g.sync_d = 1;
   if (const char* env = std::getenv("OZGPU_SYNC_G")) g.sync_g = std::max(1, std::atoi(env));
   if (const char* env = std::getenv("OZGPU_SYNC_D")) g.sync_d = std::max(1, std::atoi(env));
+  g.sync_prefetch = 1;
+  if (const char* env = std::getenv("OZGPU_SYNC_PREFETCH")) g.sync_prefetch = std::atoi(env);
 }
 
 // Diagnostics exactly as the reference accumulates them (scheme.cpp:246-359).

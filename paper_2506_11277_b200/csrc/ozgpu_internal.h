@@ -41,7 +41,7 @@ struct GemmArgs {
   // sync_d groups back, for its first sync_steps k-steps (all clusters run at
   // least that many).  sync = 64 zeroed counters, 128 bytes apart; null = off.
   int* sync;
-  int sync_steps, sync_g, sync_d, sync_clusters;
+  int sync_steps, sync_g, sync_d, sync_clusters, sync_prefetch;
   int32_t* planes;    // [nchunks][m][ldp] int32 chunk sums
   int64_t plane_stride;
   int64_t ldp;
