@@ -987,14 +987,33 @@ void host_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double
       OZ_CUDA(cudaEventRecord(a_in[i], ctx->h2d_stream));
       mark("h2d A" + std::to_string(i), ctx->h2d_stream);
     };
-    copy_a(0);
-    for (size_t j = 0; j < nc; ++j) {  // panel j: k x nj, dense at db + k * c0
+    auto copy_b = [&](size_t j) {  // panel j: k x nj, dense at db + k * c0
       h2d(db + k * cb[j], b + cb[j], k, cb[j + 1] - cb[j], ldb, ctx->h2d_stream);
       b_in[j] = next_event();
       OZ_CUDA(cudaEventRecord(b_in[j], ctx->h2d_stream));
       mark("h2d B" + std::to_string(j), ctx->h2d_stream);
+    };
+    // Default (OZGPU_PIPE_MODE=rect): A blocks and B panels alternate on the copy
+    // stream (A0 B0 B1 A1 B2 A2 ...) and each arrival releases the rectangle
+    // of C it completes (a growing square), so the tensor cores are fed
+    // while the inputs are still crossing PCIe
+    const char* pm = std::getenv("OZGPU_PIPE_MODE");
+    const bool rect = !(pm && std::string(pm) == "panels");  // measured 36.0 vs 37.0 ms at 8192^3
+    std::vector<std::pair<char, size_t>> arrivals;
+    if (rect) {
+      size_t ia = 0, jb = 0;
+      arrivals.push_back({'A', ia++});
+      while (ia < nr || jb < nc) {
+        if (jb < nc) arrivals.push_back({'B', jb++});
+        if (jb < nc && jb == 1) arrivals.push_back({'B', jb++});
+        if (ia < nr) arrivals.push_back({'A', ia++});
+      }
+      for (auto& ar : arrivals) ar.first == 'A' ? copy_a(ar.second) : copy_b(ar.second);
+    } else {
+      copy_a(0);
+      for (size_t j = 0; j < nc; ++j) copy_b(j);
+      for (size_t i = 1; i < nr; ++i) copy_a(i);
     }
-    for (size_t i = 1; i < nr; ++i) copy_a(i);
     int64_t launches = 0;
     auto slice_a = [&](size_t i) {
       OZ_CUDA(cudaStreamWaitEvent(st, a_in[i], 0));
@@ -1017,13 +1036,46 @@ void host_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double
                                 cudaMemcpyDeviceToHost, ctx->d2h_stream));
       mark("d2h " + tag, ctx->d2h_stream);
     };
-    slice_a(0);
-    for (size_t j = 0; j < nc; ++j) {
+    auto slice_b = [&](size_t j) {
       const int64_t nj = cb[j + 1] - cb[j];
       OZ_CUDA(cudaStreamWaitEvent(st, b_in[j], 0));
       OZ_CUDA(launch_slice_cols(db + k * cb[j], nj, k, nj, kp, t, p.slices_b, p.mode,
                                 slB + cb[j] * kp, 0, qb + cb[j], colmax + cb[j], status, st,
                                 &launches, n * kp));
+    };
+    if (rect) {
+      size_t na = 0, nbp = 0;  // A blocks / B panels sliced so far
+      for (size_t q = 0; q < arrivals.size(); ++q) {
+        const auto& ar = arrivals[q];
+        const bool last = q + 1 == arrivals.size();
+        if (ar.first == 'A') {
+          slice_a(ar.second);
+          na = ar.second + 1;
+          if (nbp == 0) continue;
+          const size_t i = ar.second;
+          if (last && nbp == nc) {  // final row block: two column halves shorten the D2H tail
+            for (size_t j = 0; j + 1 < cl.size(); ++j) block(rb[i], rb[i + 1], cl[j], cl[j + 1]);
+          } else {
+            block(rb[i], rb[i + 1], 0, cb[nbp]);
+          }
+        } else {
+          slice_b(ar.second);
+          nbp = ar.second + 1;
+          if (na == 0) continue;
+          const size_t j = ar.second;
+          if (last && na == nr && na > 1) {  // final column panel: split its rows
+            const size_t half = nr / 2;
+            block(rb[0], rb[half], cb[j], cb[j + 1]);
+            block(rb[half], rb[nr], cb[j], cb[j + 1]);
+          } else {
+            block(rb[0], rb[na], cb[j], cb[j + 1]);
+          }
+        }
+      }
+    } else {
+    slice_a(0);
+    for (size_t j = 0; j < nc; ++j) {
+      slice_b(j);
       block(rb[0], rb[1], cb[j], cb[j + 1]);
     }
     for (size_t i = 1; i < nr; ++i) {
@@ -1033,6 +1085,7 @@ void host_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double
       } else {
         block(rb[i], rb[i + 1], 0, n);
       }
+    }
     }
     ctx->launches += launches;
     int hs = 0;

@@ -353,8 +353,10 @@ def test_error_bound_matches_reference_and_contains(oz, ref):
     assert oz.kappa(a, oz.BlockOrientation.ROWS) == ref.ref_scaling_profile(a, b)[0]
 
 
-@pytest.mark.parametrize("rows,panels,last", [("4", "2", "2"), ("3", "4", "3"), ("8", "1", "1")])
-def test_blocked_host_pipeline_is_bitwise_identical(oz, rows, panels, last, monkeypatch):
+@pytest.mark.parametrize("rows,panels,last,mode", [("4", "2", "2", "panels"), ("3", "4", "3", "panels"),
+                                                   ("8", "1", "1", "panels"), ("4", "4", "2", "rect"),
+                                                   ("3", "5", "2", "rect")])
+def test_blocked_host_pipeline_is_bitwise_identical(oz, rows, panels, last, mode, monkeypatch):
     """ozgpu_dgemm's blocked H2D / compute / D2H pipeline (row blocks, B
     column panels for the first block, split last block) returns exactly the
     unblocked result on a ragged shape, for several blockings."""
@@ -370,6 +372,7 @@ def test_blocked_host_pipeline_is_bitwise_identical(oz, rows, panels, last, monk
     monkeypatch.setenv("OZGPU_PIPE_ROWS", rows)
     monkeypatch.setenv("OZGPU_PIPE_PANELS", panels)
     monkeypatch.setenv("OZGPU_PIPE_LAST", last)
+    monkeypatch.setenv("OZGPU_PIPE_MODE", mode)
     got = oz.multiply(a, b, cfg, plan).c
     assert bits_equal(got, want), mismatch_report(got, want)
 
