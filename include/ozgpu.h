@@ -9,7 +9,8 @@
  *   OZGPU_OK 0, OZGPU_INVALID_ARGUMENT 1 (std::invalid_argument),
  *   OZGPU_DOMAIN_ERROR 2 (std::domain_error), OZGPU_DEVICE_ERROR 3,
  *   OZGPU_INFEASIBLE 4 (SelectionInfeasible), OZGPU_OVERFLOW 5
- *   (MmaOverflowError).  ozgpu_last_error() returns the calling thread's
+ *   (MmaOverflowError), OZGPU_IO_ERROR 6 (std::runtime_error of the matrix
+ *   file functions).  ozgpu_last_error() returns the calling thread's
  *   message for the last failing call, worded like the reference's.
  *
  * Enumerations match the reference headers:
@@ -38,6 +39,7 @@ extern "C" {
 #define OZGPU_DEVICE_ERROR 3
 #define OZGPU_INFEASIBLE 4
 #define OZGPU_OVERFLOW 5
+#define OZGPU_IO_ERROR 6
 
 #define OZGPU_MAX_LEVELS 128
 
@@ -208,6 +210,14 @@ void ozgpu_random_uniform(int64_t m, int64_t n, uint64_t seed, double lo, double
 /* gen_kappa_d, proj/src/generators.cpp:103-140 */
 void ozgpu_gen_kappa_d(int64_t n, double kappa_d, uint64_t seed, int rotate, double* a_out,
                        double* b_out);
+
+/* ---- "ozm1" matrix files (proj/include/ozmul/io.hpp:26-40; io.cpp:51-95) ----
+ * format: 0 kHex (16 hex digits of the binary64 bits, bit-exact), 1 kDec
+ * (shortest round-trip decimal).  Matrices are row-major. */
+int ozgpu_matrix_file_shape(const char* path, int64_t* rows, int64_t* cols);
+int ozgpu_read_matrix_file(const char* path, int format, int64_t rows, int64_t cols, double* out);
+int ozgpu_write_matrix_file(const char* path, int format, int64_t rows, int64_t cols,
+                            const double* a, int64_t ld);
 
 #ifdef __cplusplus
 }

@@ -307,6 +307,40 @@ def ref_random_uniform(m, n, seed, lo=0.0, hi=1.0):
     return out
 
 
+def _ozm_tool():
+    tool = os.path.join(os.path.dirname(REF_PATH), "ozm_tool")
+    if not os.path.exists(tool):
+        have_ref()
+    if not os.path.exists(tool):
+        raise RuntimeError("oracle/_ref/ozm_tool is not built")
+    return tool
+
+
+def ref_write_matrix_file(path, a, fmt=0):
+    """The reference's write_matrix_file (io.cpp:97-103) via oracle/_ref/ozm_tool
+    (a separate process: the reference's stream code is not called in-process);
+    fmt 0 hex, 1 decimal."""
+    import subprocess
+    import tempfile
+    a = _f64(a)
+    with tempfile.NamedTemporaryFile(suffix=".f64") as raw:
+        raw.write(a.tobytes())
+        raw.flush()
+        subprocess.run([_ozm_tool(), "w", "hex" if fmt == 0 else "dec", str(a.shape[0]),
+                        str(a.shape[1]), raw.name, str(path)], check=True)
+
+
+def ref_read_matrix_file(path, fmt=0):
+    """The reference's read_matrix_file (io.cpp:65-69) -> ndarray."""
+    import subprocess
+    import tempfile
+    with tempfile.NamedTemporaryFile(suffix=".f64") as raw:
+        r = subprocess.run([_ozm_tool(), "r", "hex" if fmt == 0 else "dec", str(path), raw.name],
+                           check=True, capture_output=True, text=True)
+        rows, cols = (int(v) for v in r.stdout.split())
+        return np.fromfile(raw.name, dtype=np.float64).reshape(rows, cols)
+
+
 def ref_gen_kappa_d(n, kappa_d, seed, rotate):
     a, b = np.empty((n, n)), np.empty((n, n))
     _rc(ref().ozref_gen_kappa_d(n, kappa_d, seed, int(rotate), _dp(a), _dp(b)))

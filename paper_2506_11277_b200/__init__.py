@@ -182,8 +182,13 @@ class MmaOverflowError(OzmulError, RuntimeError):
     code = 5
 
 
+class MatrixIOError(OzmulError, RuntimeError):
+    """std::runtime_error of the reference's matrix file functions (io.cpp)."""
+    code = 6
+
+
 _ERRORS = {1: InvalidArgument, 2: DomainError, 3: DeviceError, 4: SelectionInfeasible,
-           5: MmaOverflowError}
+           5: MmaOverflowError, 6: MatrixIOError}
 
 
 def _check(rc: int) -> None:
@@ -575,6 +580,38 @@ def gen_kappa_d(n: int, kappa_d: float, seed: int, rotate: bool):
     b = np.empty((n, n), dtype=np.float64)
     _lib.ozgpu_gen_kappa_d(n, kappa_d, seed, int(rotate), _dp(a), _dp(b))
     return a, b
+
+
+# ------------------------------------------------- ozm1 matrix files (io.hpp)
+
+
+class MatrixFormat(enum.IntEnum):
+    HEX = 0  # kHex: 16 hex digits of the binary64 bit pattern (bit-exact)
+    DEC = 1  # kDec: shortest round-trip decimal
+
+
+_sig("ozgpu_matrix_file_shape", ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(_I64),
+     ctypes.POINTER(_I64))
+_sig("ozgpu_read_matrix_file", ctypes.c_int, ctypes.c_char_p, ctypes.c_int, _I64, _I64, _DP)
+_sig("ozgpu_write_matrix_file", ctypes.c_int, ctypes.c_char_p, ctypes.c_int, _I64, _I64, _DP,
+     _I64)
+
+
+def read_matrix_file(path, fmt: MatrixFormat = MatrixFormat.HEX) -> np.ndarray:
+    """read_matrix_file (io.hpp:33): an "ozm1 <rows> <cols>" file -> row-major f64."""
+    rows, cols = _I64(), _I64()
+    _check(_lib.ozgpu_matrix_file_shape(os.fsencode(path), ctypes.byref(rows), ctypes.byref(cols)))
+    out = np.empty((rows.value, cols.value), dtype=np.float64)
+    _check(_lib.ozgpu_read_matrix_file(os.fsencode(path), int(fmt), rows.value, cols.value,
+                                       _dp(out)))
+    return out
+
+
+def write_matrix_file(path, a, fmt: MatrixFormat = MatrixFormat.HEX) -> None:
+    """write_matrix_file (io.hpp:35)."""
+    a = _f64(a)
+    _check(_lib.ozgpu_write_matrix_file(os.fsencode(path), int(fmt), a.shape[0], a.shape[1],
+                                        _dp(a), a.shape[1]))
 
 
 # ------------------------------------------------------------ stage timing

@@ -33,6 +33,13 @@ namespace {
 
 thread_local std::string g_error;
 
+}  // namespace
+
+// for the C-ABI entry points defined in other translation units (ozgpu_io.cpp)
+void set_last_error(const std::string& msg) { g_error = msg; }
+
+namespace {
+
 struct DeviceError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
