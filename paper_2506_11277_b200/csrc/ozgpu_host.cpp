@@ -117,6 +117,7 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
 struct ozgpu_ctx {
   int device = 0;
   int num_sms = 0;
+  size_t total_mem = 0;
   cudaStream_t stream = nullptr;
   std::mutex mu;
   std::atomic<int64_t> launches{0};
@@ -172,6 +173,7 @@ void init_ctx(ozgpu_ctx* ctx, int device) {
                       ") is not sm_100: kernels are built for sm_100a only");
   ctx->device = device;
   ctx->num_sms = prop.multiProcessorCount;
+  ctx->total_mem = prop.totalGlobalMem;
   OZ_CUDA(cudaSetDevice(device));
   OZ_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
   void* fn = nullptr;
@@ -595,9 +597,7 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
     if (const char* env = std::getenv("OZGPU_PLANE_BUDGET_GB")) {
       budget = std::atof(env) * 1073741824.0;
     } else {
-      size_t free_b = 0, total_b = 0;
-      OZ_CUDA(cudaMemGetInfo(&free_b, &total_b));
-      budget = 0.25 * static_cast<double>(total_b);
+      budget = 0.25 * static_cast<double>(ctx->total_mem);  // no per-call driver query
     }
     if (plane_bytes > budget) {
       const double per_row = 4.0 * static_cast<double>(cp.chunks.size()) * ldp_b;
