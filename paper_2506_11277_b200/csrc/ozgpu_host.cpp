@@ -932,7 +932,15 @@ void host_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double
   if (pipeline) {
     // measured on B200 (PCIe ~52 GB/s each way) at 8192^3 (12,12): 4 row
     // blocks with the first one in 4 column panels, the last in 2 halves
-    const int nblk = std::max(1, env_int("OZGPU_PIPE_ROWS", 4));
+    // tall-skinny (B much smaller than A): the C row blocks' copy-back
+    // dominates, so ~64 MiB row blocks of A (measured 65536 x 2048^2: 25.5 ms
+    // with 16 blocks vs 31.7 ms with 4); square shapes keep 4 x 4
+    int rows_default = 4;
+    if (8 * n <= m) {
+      const double a_bytes = 8.0 * static_cast<double>(m) * static_cast<double>(k);
+      rows_default = static_cast<int>(std::clamp(a_bytes / (64.0 * 1048576.0), 4.0, 32.0));
+    }
+    const int nblk = std::max(1, env_int("OZGPU_PIPE_ROWS", rows_default));
     const int npan = std::max(1, env_int("OZGPU_PIPE_PANELS", 4));
     const int nlast = std::max(1, env_int("OZGPU_PIPE_LAST", 2));
     if (!ctx->h2d_stream) {
