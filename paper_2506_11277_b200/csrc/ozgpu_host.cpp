@@ -559,7 +559,9 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
     // the two HBM-bound chains overlap (their tails and the short memsets
     // hide each other); joined before the GEMM.  OZGPU_SLICE_FORK=0: serial.
     const char* fv = std::getenv("OZGPU_SLICE_FORK");
-    const bool fork = !(fv && std::string(fv) == "0") && m > 0 && n > 0;
+    // (small operands: the fork / join costs more than the overlap saves)
+    const bool fork = !(fv && std::string(fv) == "0") && m > 0 && n > 0 &&
+                      (m + n) * k >= (int64_t{8} << 20);
     cudaStream_t sb_st = st;
     if (fork) {
       if (!ctx->fork_stream) {
