@@ -329,69 +329,6 @@ __global__ void __launch_bounds__(256, MINB) slice_rows_stream_kernel(
   }
 }
 
-// Single-pass row slicing with the row held in registers: a CTA of 256
-// threads takes one row of up to 256 * NPT entries per iteration, each thread
-// NPT / 8 groups of 8 consecutive entries (16-byte loads), reduces the row
-// maximum through shuffles and shared memory, and slices straight from its
-// registers -- A crosses HBM once.  Opt-in (OZGPU_SLICE_ROWS=reg).
-template <int T, int NPT>
-__global__ void __launch_bounds__(256) slice_rows_reg_kernel(
-    const double* __restrict__ a, int64_t lda, int64_t m, int64_t k, int64_t kp, int64_t plane,
-    int count, int8_t* __restrict__ out, int* __restrict__ scales, int* __restrict__ status) {
-  constexpr int G = NPT / 8;
-  __shared__ unsigned long long red[8];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t groups = kp / 8;
-  int bad = 0;
-  for (int64_t row = blockIdx.x; row < m; row += gridDim.x) {
-    const double* ar = a + row * lda;
-    double v[G][8];
-    unsigned long long mx = 0;
-#pragma unroll
-    for (int gi = 0; gi < G; ++gi) {
-      const int64_t j0 = (static_cast<int64_t>(gi) * 256 + threadIdx.x) * 8;
-      if (j0 + 8 <= k) {
-        const double2* p2 = reinterpret_cast<const double2*>(ar + j0);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const double2 t2 = __ldcs(p2 + u);
-          v[gi][2 * u] = t2.x;
-          v[gi][2 * u + 1] = t2.y;
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) v[gi][e] = j0 + e < k ? __ldcs(ar + j0 + e) : 0.0;
-      }
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        bad |= dirty(v[gi][e]);
-        const unsigned long long b = abs_bits(v[gi][e]);
-        mx = b > mx ? b : mx;
-      }
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const unsigned long long t = __shfl_xor_sync(0xFFFFFFFFu, mx, o);
-      mx = t > mx ? t : mx;
-    }
-    if (lane == 0) red[warp] = mx;
-    __syncthreads();
-    unsigned long long rmax = 0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) rmax = red[w] > rmax ? red[w] : rmax;
-    const int q = scale_from_maxbits(rmax);
-    if (threadIdx.x == 0) scales[row] = q;
-#pragma unroll
-    for (int gi = 0; gi < G; ++gi) {
-      const int64_t g = static_cast<int64_t>(gi) * 256 + threadIdx.x;
-      if (g < groups) emit8_trunc_i8<T>(v[gi], q, count, out, plane, row * kp + g * 8);
-    }
-    __syncthreads();  // red[] is rewritten by the next row
-  }
-  bad = __reduce_or_sync(0xFFFFFFFFu, bad);
-  if (lane == 0 && bad) atomicOr(status, bad);
-}
-
 // 128 (k) x 32 (n) tile transpose-and-slice into K-major [l][n][kp] int8.
 // Smem holds the tile column-major in 16-byte units with an XOR swizzle so
 // both the row-wise fill and the 8-entry column reads are conflict-light.
@@ -462,20 +399,6 @@ static int launch_rows_fast_t(const double* a, int64_t lda, int64_t m, int64_t k
                                int64_t plane, int count, int8_t* out, int* scales, int* status,
                                cudaStream_t st) {
   const bool vec = (reinterpret_cast<uintptr_t>(a) & 15) == 0 && (lda & 1) == 0;
-  const char* rv = std::getenv("OZGPU_SLICE_ROWS");
-  if (vec && rv && std::string(rv) == "reg" && kp <= 256 * 32) {
-    const int grid_r = static_cast<int>(std::min<int64_t>(m, 148 * 8));
-    if (kp <= 256 * 8)
-      slice_rows_reg_kernel<T, 8><<<grid_r, 256, 0, st>>>(a, lda, m, k, kp, plane, count, out,
-                                                         scales, status);
-    else if (kp <= 256 * 16)
-      slice_rows_reg_kernel<T, 16><<<grid_r, 256, 0, st>>>(a, lda, m, k, kp, plane, count, out,
-                                                          scales, status);
-    else
-      slice_rows_reg_kernel<T, 32><<<grid_r, 256, 0, st>>>(a, lda, m, k, kp, plane, count, out,
-                                                          scales, status);
-    return 1;
-  }
   const int grid = grid_for(m, 8, 148 * 16);
   const int grid2 = grid_for(m * (kp / 8), 256, 148 * 16);
   // 4 CTAs / SM (64 registers, measured ~3% faster than 3 / SM on B200)
