@@ -450,6 +450,33 @@ def main():
                           "ms_per_step": sms})
         line["sweep"] = sweep
 
+    # context only (off the product path): cuBLAS DGEMM on the same device
+    # operands, the native FP64 rate the emulation is compared with
+    # (PAPER.md:548 reports 7.6x over it at s=3 on B200)
+    if world == 1 and not args.no_sweep:
+        try:
+            ad, bd = a_d[:m, :k], b_d[:k, :n]
+            torch.matmul(ad, bd)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            reps = 3
+            e0.record()
+            for _ in range(reps):
+                torch.matmul(ad, bd)
+            e1.record()
+            torch.cuda.synchronize()
+            dms = e0.elapsed_time(e1) / reps
+            line["fp64_dgemm_reference"] = {
+                "api": "torch.matmul float64 (cuBLAS DGEMM), same inputs, not on the product path",
+                "tflops": flops_rank / (dms * 1e-3) / 1e12, "ms": dms,
+                "speedup_estimator_slices": (flops_rank / (ms * 1e-3) / 1e12) /
+                                            (flops_rank / (dms * 1e-3) / 1e12),
+                "speedup_s3": (line["sweep"][0]["tflops"] / world) /
+                              (flops_rank / (dms * 1e-3) / 1e12) if line.get("sweep") else None}
+        except Exception as e:  # context only: never fail the bench line
+            line["fp64_dgemm_reference"] = {"error": repr(e)}
+
     # e2e through the host-pointer C-ABI call (pinned host buffers)
     if not args.no_e2e:
         a_p = torch.from_numpy(a_h).pin_memory().numpy()
