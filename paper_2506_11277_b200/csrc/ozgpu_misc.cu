@@ -318,13 +318,15 @@ __device__ __forceinline__ int64_t mad_run(int64_t a, uint32_t r, int32_t s) {
 template <int BATCH, int MINB, int W>
 __global__ void __launch_bounds__(256, MINB) combine_hilo_v4_kernel(const CombineArgs p,
                                                                     const HiloProgram hp) {
-  const int64_t groups_per_row = p.n / 4;
-  const int64_t total = static_cast<int64_t>(p.m) * groups_per_row;
+  // 2-D grid: x covers a row's 4-column groups, y strides over rows (no
+  // per-element index division)
+  const int groups_per_row = p.n / 4;
   const bool vec_c = (p.ldc & 1) == 0 && (reinterpret_cast<uintptr_t>(p.c) & 15) == 0;
   const int64_t stride4 = p.plane_stride / 4;
-  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
-       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t i = idx / groups_per_row, j = (idx - i * groups_per_row) * 4;
+  const int jg = blockIdx.x * blockDim.x + threadIdx.x;
+  if (jg >= groups_per_row) return;
+  for (int64_t i = blockIdx.y; i < p.m; i += gridDim.y) {
+    const int64_t j = static_cast<int64_t>(jg) * 4;
     const int4* src = reinterpret_cast<const int4*>(p.planes + i * p.ldp + j);
     uint64_t v[4][W];
 #pragma unroll
@@ -665,12 +667,15 @@ cudaError_t launch_combine_exact(const CombineArgs& args, int words, const Chunk
           // {4,6,8,12} x {2,3,4} on B200 (OZGPU_COMBINE_CFG=83 selects 8 / 3)
           const char* cv = std::getenv("OZGPU_COMBINE_CFG");
           const int cfg = cv ? std::atoi(cv) : 44;
+          const int gx = (args.n / 4 + 255) / 256;
+          const int gy = static_cast<int>(std::min<int64_t>(args.m, std::max(1, 148 * 16 / gx)));
+          const dim3 grid2(gx, gy);
           if (w3)
-            combine_hilo_v4_kernel<4, 3, 3><<<grid, 256, 0, st>>>(args, hp);
+            combine_hilo_v4_kernel<4, 3, 3><<<grid2, 256, 0, st>>>(args, hp);
           else if (cfg == 83)
-            combine_hilo_v4_kernel<8, 3, 2><<<grid, 256, 0, st>>>(args, hp);
+            combine_hilo_v4_kernel<8, 3, 2><<<grid2, 256, 0, st>>>(args, hp);
           else
-            combine_hilo_v4_kernel<4, 4, 2><<<grid, 256, 0, st>>>(args, hp);
+            combine_hilo_v4_kernel<4, 4, 2><<<grid2, 256, 0, st>>>(args, hp);
           ++*launches;
           return cudaGetLastError();
         }

@@ -304,6 +304,32 @@ OZ_HD double pow2_normal(long x) { return bits_dbl(static_cast<uint64_t>(x + 102
 //   Everything else takes round_i128.
 OZ_HD double round_hilo(uint64_t hi, uint64_t lo, long e) {
   const int64_t h = static_cast<int64_t>(hi);
+  const int64_t l = static_cast<int64_t>(lo);
+  if (h == (l >> 63) && e >= -1000 && e <= 900) {
+    // v fits in int64 (few diagonals, e.g. s = 3): one correctly rounded
+    // conversion (exact below 2^51 via the magic number), then an exact
+    // power-of-two scale -- the result is normal for these e
+    if (l == 0) return 0.0;
+    double d;
+    if (l < (int64_t{1} << 51) && l > -(int64_t{1} << 51)) {
+#ifdef __CUDA_ARCH__
+      d = __dsub_rn(bits_dbl(0x4338000000000000ULL + static_cast<uint64_t>(l)), 6755399441055744.0);
+#else
+      d = bits_dbl(0x4338000000000000ULL + static_cast<uint64_t>(l)) - 6755399441055744.0;
+#endif
+    } else {
+#ifdef __CUDA_ARCH__
+      d = __ll2double_rn(l);
+#else
+      d = static_cast<double>(l);
+#endif
+    }
+#ifdef __CUDA_ARCH__
+    return __dmul_rn(d, pow2_normal(e));
+#else
+    return d * pow2_normal(e);
+#endif
+  }
   const bool big = (h >= 4 || h <= -5) && h < (int64_t{1} << 51) && h > -(int64_t{1} << 51);
   if (big && e >= -1034 && e <= 900) {
     const uint64_t lr = (lo >> 12) | ((lo & 0xFFF) != 0);
