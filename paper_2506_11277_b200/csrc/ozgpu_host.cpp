@@ -1545,6 +1545,13 @@ int ozgpu_dgemm_device(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const do
       std::string gkey(key);
       for (char** ev = environ; ev && *ev; ++ev)
         if (std::strncmp(*ev, "OZGPU_", 6) == 0) gkey += std::string("|") + *ev;
+      if (ctx->graphs.size() >= 64 && !ctx->graphs.count(gkey)) {  // bound the cache
+        for (auto& kv : ctx->graphs) {
+          if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+          for (void* pp : kv.second.pinned) cudaFreeHost(pp);
+        }
+        ctx->graphs.clear();
+      }
       auto& e = ctx->graphs[gkey];
       const uint64_t gen = g_workspace_gen.load();
       if (e.exec && e.gen == gen) {
