@@ -1546,6 +1546,7 @@ int ozgpu_dgemm_device(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const do
       for (char** ev = environ; ev && *ev; ++ev)
         if (std::strncmp(*ev, "OZGPU_", 6) == 0) gkey += std::string("|") + *ev;
       if (ctx->graphs.size() >= 64 && !ctx->graphs.count(gkey)) {  // bound the cache
+        OZ_CUDA(cudaDeviceSynchronize());  // pinned table copies may still be in flight
         for (auto& kv : ctx->graphs) {
           if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
           for (void* pp : kv.second.pinned) cudaFreeHost(pp);
@@ -1561,6 +1562,7 @@ int ozgpu_dgemm_device(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const do
         return;
       }
       if (e.exec) {  // stale: the workspace moved
+        OZ_CUDA(cudaDeviceSynchronize());  // its pinned table copies may still be in flight
         cudaGraphExecDestroy(e.exec);
         e.exec = nullptr;
         for (void* pp : e.pinned) cudaFreeHost(pp);
