@@ -216,9 +216,12 @@ __device__ __forceinline__ void emit8_trunc_i8(const double (&v)[8], int q, int 
     uint64_t w[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
+      // branch-free: PTX 64-bit shifts clamp amounts >= 64 to a zero result
       const int sh = WB * (j + 1) - lsb[e];
-      uint64_t x = sh >= 0 ? (sh < 64 ? (sig[e] << sh) : 0ULL) : (sh > -64 ? (sig[e] >> -sh) : 0ULL);
-      w[e] = x & WMASK;
+      uint64_t l, r;
+      asm("shl.b64 %0, %1, %2;" : "=l"(l) : "l"(sig[e]), "r"(static_cast<uint32_t>(max(sh, 0))));
+      asm("shr.b64 %0, %1, %2;" : "=l"(r) : "l"(sig[e]), "r"(static_cast<uint32_t>(max(-sh, 0))));
+      w[e] = (sh >= 0 ? l : r) & WMASK;
     }
 #pragma unroll
     for (int i = 0; i < SPW; ++i) {
