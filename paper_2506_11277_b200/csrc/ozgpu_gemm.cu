@@ -747,7 +747,8 @@ cudaError_t launch_gemm_i8_pair(const CUtensorMap* tma, const CUtensorMap* tmb,
   if (pairs < 1) return cudaSuccess;
   const char* sv = std::getenv("OZGPU_PAIR_STAGES");
   const int stages = sv ? std::atoi(sv) : 6;
-  cudaError_t e0 = stages == 6 ? launch_pair_t<6>(tma, tmb, args, pairs, st)
+  cudaError_t e0 = stages == 7 ? launch_pair_t<7>(tma, tmb, args, pairs, st)
+                 : stages == 6 ? launch_pair_t<6>(tma, tmb, args, pairs, st)
                  : stages == 5 ? launch_pair_t<5>(tma, tmb, args, pairs, st)
                  : stages == 3 ? launch_pair_t<3>(tma, tmb, args, pairs, st)
                                : launch_pair_t<4>(tma, tmb, args, pairs, st);
