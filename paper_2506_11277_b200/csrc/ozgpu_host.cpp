@@ -934,16 +934,13 @@ void host_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double
   if (pipeline) {
     // measured on B200 (PCIe ~52 GB/s each way) at 8192^3 (12,12): 4 row
     // blocks with the first one in 4 column panels, the last in 2 halves
-    // tall-skinny (B much smaller than A): the C row blocks' copy-back
-    // dominates, so ~64 MiB row blocks of A (measured 65536 x 2048^2: 25.5 ms
-    // with 16 blocks vs 31.7 ms with 4); square shapes keep 4 x 4
-    int rows_default = 4;
-    if (8 * n <= m) {
-      const double a_bytes = 8.0 * static_cast<double>(m) * static_cast<double>(k);
-      rows_default = static_cast<int>(std::clamp(a_bytes / (64.0 * 1048576.0), 4.0, 32.0));
-    }
+    // ~2048-row blocks of A and ~2048-column panels of B (at least 4 each):
+    // measured 8192^3 4 x 4 (36.0 ms), 16384^3 8 x 8 (295 vs 307 ms with
+    // 4 x 4), 65536 x 2048^2 32 row blocks (25.4 vs 31.7 ms with 4)
+    const int rows_default = static_cast<int>(std::clamp<int64_t>((m + 1024) / 2048, 4, 32));
+    const int pan_default = static_cast<int>(std::clamp<int64_t>((n + 1024) / 2048, 4, 16));
     const int nblk = std::max(1, env_int("OZGPU_PIPE_ROWS", rows_default));
-    const int npan = std::max(1, env_int("OZGPU_PIPE_PANELS", 4));
+    const int npan = std::max(1, env_int("OZGPU_PIPE_PANELS", pan_default));
     const int nlast = std::max(1, env_int("OZGPU_PIPE_LAST", 2));
     if (!ctx->h2d_stream) {
       OZ_CUDA(cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
