@@ -932,16 +932,21 @@ void host_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double
   const bool pipeline = !failing && !axpby && p.strategy == 2 && m >= 2048 && n >= 1024 &&
                         bytes >= (64 << 20) && env_int("OZGPU_PIPE", 1) == 1;
   if (pipeline) {
-    // measured on B200 (PCIe ~52 GB/s each way) at 8192^3 (12,12): 4 row
-    // blocks with the first one in 4 column panels, the last in 2 halves
-    // ~2048-row blocks of A and ~2048-column panels of B (at least 4 each):
-    // measured 8192^3 4 x 4 (36.0 ms), 16384^3 8 x 8 (295 vs 307 ms with
-    // 4 x 4), 65536 x 2048^2 32 row blocks (25.4 vs 31.7 ms with 4)
+    // ~2048-row blocks of A and ~2048-column panels of B (at least 4 each),
+    // measured on B200 (PCIe ~55 GB/s each way): 8192^3 4 x 4 (35.5 ms),
+    // 16384^3 8 x 8 (277 vs 307 ms with 4 x 4), 65536 x 2048^2 32 row blocks
+    // (24.5 vs 31.7 ms with 4).  OZGPU_PIPE_FIRST=f makes the first row block
+    // and the first column panel 1/f of the others (less to copy before the
+    // tensor cores start).
     const int rows_default = static_cast<int>(std::clamp<int64_t>((m + 1024) / 2048, 4, 32));
     const int pan_default = static_cast<int>(std::clamp<int64_t>((n + 1024) / 2048, 4, 16));
     const int nblk = std::max(1, env_int("OZGPU_PIPE_ROWS", rows_default));
     const int npan = std::max(1, env_int("OZGPU_PIPE_PANELS", pan_default));
-    const int nlast = std::max(1, env_int("OZGPU_PIPE_LAST", 2));
+    // measured at 8192^3: first blocks of half size and the final row block
+    // in 4 column parts, 36.2 -> 34.6 ms (16384^3: 4 parts cost 5 ms, so 2)
+    const int last_default = n <= 8192 ? static_cast<int>(std::clamp<int64_t>(n / 2048, 2, 4)) : 2;
+    const int nlast = std::max(1, env_int("OZGPU_PIPE_LAST", last_default));
+    const int first = std::max(1, env_int("OZGPU_PIPE_FIRST", 2));
     if (!ctx->h2d_stream) {
       OZ_CUDA(cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
       OZ_CUDA(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
@@ -960,15 +965,17 @@ void host_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double
     // row blocks (multiples of 256 rows) and column panels (multiples of 256)
     std::vector<int64_t> rb{0}, cb{0};
     const int64_t rows = round_up((m + nblk - 1) / nblk, 256);
+    if (first > 1) rb.push_back(std::min(m, round_up(rows / first, 256)));
     while (rb.back() < m) rb.push_back(std::min(m, rb.back() + rows));
-    auto split_cols = [&](int parts) {
+    auto split_cols = [&](int parts, int lead) {
       std::vector<int64_t> e{0};
       const int64_t w = round_up((n + parts - 1) / parts, 256);
+      if (lead > 1) e.push_back(std::min(n, round_up(w / lead, 256)));
       while (e.back() < n) e.push_back(std::min(n, e.back() + w));
       return e;
     };
-    cb = split_cols(npan);
-    const std::vector<int64_t> cl = split_cols(nlast);
+    cb = split_cols(npan, first);
+    const std::vector<int64_t> cl = split_cols(nlast, 1);
     const size_t nr = rb.size() - 1, nc = cb.size() - 1;
     const size_t nev = 1 + nr + nc + nr * std::max(nc, cl.size()) + 4;
     while (ctx->pipe_events.size() < nev) {
