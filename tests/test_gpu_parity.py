@@ -353,13 +353,15 @@ def test_error_bound_matches_reference_and_contains(oz, ref):
     assert oz.kappa(a, oz.BlockOrientation.ROWS) == ref.ref_scaling_profile(a, b)[0]
 
 
-@pytest.mark.parametrize("rows,panels,last,mode", [("4", "2", "2", "panels"), ("3", "4", "3", "panels"),
-                                                   ("8", "1", "1", "panels"), ("4", "4", "2", "rect"),
-                                                   ("3", "5", "2", "rect")])
-def test_blocked_host_pipeline_is_bitwise_identical(oz, rows, panels, last, mode, monkeypatch):
+@pytest.mark.parametrize("rows,panels,last,mode,first", [
+    ("4", "2", "2", "panels", "1"), ("3", "4", "3", "panels", "2"), ("8", "1", "1", "panels", "1"),
+    ("4", "4", "2", "rect", "1"), ("3", "5", "2", "rect", "2"), ("4", "4", "4", "rect", "2"),
+    ("5", "3", "3", "rect", "3")])
+def test_blocked_host_pipeline_is_bitwise_identical(oz, rows, panels, last, mode, first, monkeypatch):
     """ozgpu_dgemm's blocked H2D / compute / D2H pipeline (row blocks, B
-    column panels for the first block, split last block) returns exactly the
-    unblocked result on a ragged shape, for several blockings."""
+    column panels, a smaller first block and panel, split last block)
+    returns exactly the unblocked result on a ragged shape, for several
+    blockings."""
     rng = np.random.default_rng(5)
     m, k, n = 2600, 1000, 3000
     a = uniform(m, k, rng)
@@ -373,6 +375,7 @@ def test_blocked_host_pipeline_is_bitwise_identical(oz, rows, panels, last, mode
     monkeypatch.setenv("OZGPU_PIPE_PANELS", panels)
     monkeypatch.setenv("OZGPU_PIPE_LAST", last)
     monkeypatch.setenv("OZGPU_PIPE_MODE", mode)
+    monkeypatch.setenv("OZGPU_PIPE_FIRST", first)
     got = oz.multiply(a, b, cfg, plan).c
     assert bits_equal(got, want), mismatch_report(got, want)
 
