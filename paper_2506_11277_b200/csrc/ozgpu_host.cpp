@@ -965,12 +965,12 @@ void host_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double
     // row blocks (multiples of 256 rows) and column panels (multiples of 256)
     std::vector<int64_t> rb{0}, cb{0};
     const int64_t rows = round_up((m + nblk - 1) / nblk, 256);
-    if (first > 1) rb.push_back(std::min(m, round_up(rows / first, 256)));
+    if (first > 1) rb.push_back(std::min(m, std::max<int64_t>(256, round_up(rows / first, 256))));
     while (rb.back() < m) rb.push_back(std::min(m, rb.back() + rows));
     auto split_cols = [&](int parts, int lead) {
       std::vector<int64_t> e{0};
       const int64_t w = round_up((n + parts - 1) / parts, 256);
-      if (lead > 1) e.push_back(std::min(n, round_up(w / lead, 256)));
+      if (lead > 1) e.push_back(std::min(n, std::max<int64_t>(256, round_up(w / lead, 256))));
       while (e.back() < n) e.push_back(std::min(n, e.back() + w));
       return e;
     };
