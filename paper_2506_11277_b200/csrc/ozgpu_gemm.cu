@@ -135,6 +135,19 @@ __device__ __forceinline__ void decode_unit(int unit, const GemmArgs& p, bool fu
   decode_unit(unit, p, fused, tc, c0, nc, tile, mc_rank);
 }
 
+// Split-k tail: virtual unit -> (real unit, k-block range, partial?).
+__device__ __forceinline__ bool tail_range(int& unit, const GemmArgs& p, int& kb0, int& kb1) {
+  kb0 = 0;
+  kb1 = p.kblocks;
+  if (p.tail_parts == 0 || unit < p.tail_first) return false;
+  const int v = unit - p.tail_first;
+  const int r = v / p.tail_parts, part = v - r * p.tail_parts;
+  unit = p.tail_first + r;
+  kb0 = part * p.kblocks / p.tail_parts;
+  kb1 = (part + 1) * p.kblocks / p.tail_parts;
+  return true;
+}
+
 __device__ __forceinline__ int ld_acquire_gpu(const int* ptr) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
@@ -586,9 +599,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     int step = 0;               // k-steps issued by this cluster
     bool lockstep = p.sync != nullptr && leader;
     int seen = -1;
-    for (int unit = pair; unit < p.total_units; unit += npairs) {
+    for (int vunit = pair; vunit < p.total_units; vunit += npairs) {
       TileCoord tc;
-      int c0, nc;
+      int c0, nc, kb0, kb1, unit = vunit;
+      tail_range(unit, p, kb0, kb1);
       decode_unit(unit, p, false, tc, c0, nc);
       const int arow = tc.tm * 256 + static_cast<int>(rank) * 128;
       const int brow = tc.tn * kBN + static_cast<int>(rank) * 128;
@@ -597,7 +611,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       for (int pr = 0; pr < cd.npairs; ++pr) {
         const int l = cd.l0 + pr;
         const int h = cd.d + 2 - l;
-        for (int kb = 0; kb < p.kblocks; ++kb, ++step) {
+        for (int kb = kb0; kb < kb1; ++kb, ++step) {
           lockstep = lockstep_point(p, step, lockstep, seen);
           mbar_wait(&empty[stage], phase ^ 1);
           if (elect_one()) {
@@ -631,9 +645,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    for (int unit = pair; unit < p.total_units; unit += npairs) {
+    for (int vunit = pair; vunit < p.total_units; vunit += npairs) {
       TileCoord tc;
-      int c0, nc;
+      int c0, nc, kb0, kb1, unit = vunit;
+      tail_range(unit, p, kb0, kb1);
       decode_unit(unit, p, false, tc, c0, nc);
       for (int c = c0; c < c0 + nc; ++c, ++it) {
       const ChunkDesc cd = p.chunks[chunk_at(p, c)];
@@ -642,7 +657,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       mbar_wait(&tempty[acc], aphase ^ 1);
       tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * kBN;
-      const int total = cd.npairs * p.kblocks;
+      const int total = cd.npairs * (kb1 - kb0);
       for (int i = 0; i < total; ++i) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
@@ -669,9 +684,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     const uint32_t tempty_leader0 = map_to_rank(&tempty[0], 0);
     const uint32_t tempty_leader1 = map_to_rank(&tempty[1], 0);
     int it = 0;
-    for (int unit = pair; unit < p.total_units; unit += npairs) {
+    for (int vunit = pair; vunit < p.total_units; vunit += npairs) {
       TileCoord tc;
-      int c0, nc;
+      int c0, nc, kb0, kb1, unit = vunit;
+      const bool partial = tail_range(unit, p, kb0, kb1);
       decode_unit(unit, p, false, tc, c0, nc);
       for (int cpos = c0; cpos < c0 + nc; ++cpos, ++it) {
       const int c = chunk_at(p, cpos);
@@ -688,7 +704,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         uint32_t r[32];
         tmem_ld32(taddr + s0, r);
         const int col0 = tc.tn * kBN + s0;
-        if (row < p.m) {
+        if (row < p.m && partial) {  // exact integer partial sums: order-free
+          for (int v = 0; v < 32; ++v)
+            if (col0 + v < p.n && r[v] != 0u) atomicAdd(dst + col0 + v, static_cast<int>(r[v]));
+        } else if (row < p.m) {
           if (col0 + 32 <= p.n && (p.ldp & 3) == 0) {
             int4* d4 = reinterpret_cast<int4*>(dst + col0);
 #pragma unroll

@@ -737,6 +737,49 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
         g.total_units = static_cast<int>(static_cast<int64_t>(pair_tiles) * nb);
       }
       setup_lockstep(ctx, g, cp, aux, bfirst, st);
+      // Split-k tail (OZGPU_TAIL_SPLIT=0 turns it off): the R units of the
+      // last partial wave (equal-length units on C CTA pairs, R = U mod C) are
+      // each cut into P = C / R k-ranges that run side by side and add their
+      // exact int32 partial sums into the plane (zeroed here over the tail
+      // tiles' bounding box; the other tiles in the box are stored later in
+      // the same launch).  At 8192^3 (12,12): 6144 units on 74 pairs leave 2
+      // units for a whole unit time.
+      {
+        bool tail = true;
+        if (const char* env = std::getenv("OZGPU_TAIL_SPLIT")) tail = std::string(env) == "1";
+        const int clusters = std::min(ctx->num_sms / 2, g.total_units);
+        const int U = g.total_units;
+        const int R = clusters > 0 ? U % clusters : 0;
+        const int P = R ? clusters / R : 0;
+        if (tail && g.bin_first && R && P >= 2 && pair_tiles >= R && g.kblocks >= P &&
+            U >= clusters) {
+          const int G = g.group > 0 ? g.group : 8;
+          int r0 = INT32_MAX, r1 = 0, q0 = INT32_MAX, q1 = 0;
+          for (int u = U - R; u < U; ++u) {
+            const int tile = u % pair_tiles;  // the last bin (R <= pair_tiles)
+            const int group_size = G * g.tiles_n;
+            const int grp = tile / group_size, first_m = grp * G;
+            const int gsz = std::min(G, g.tiles_m - first_m);
+            const int in_group = tile - grp * group_size;
+            const int tm = first_m + in_group % gsz, tn = in_group / gsz;
+            r0 = std::min(r0, tm * 256);
+            r1 = std::max(r1, tm * 256 + 256);
+            q0 = std::min(q0, tn * 256);
+            q1 = std::max(q1, tn * 256 + 256);
+          }
+          r1 = static_cast<int>(std::min<int64_t>(r1, m));
+          q1 = static_cast<int>(std::min<int64_t>(q1, n));
+          const size_t nb = bfirst.size() - 1;
+          for (int q = bfirst[nb - 1]; q < bfirst[nb]; ++q)
+            OZ_CUDA(cudaMemset2DAsync(planes + static_cast<int64_t>(aux[q]) * plane +
+                                          static_cast<int64_t>(r0) * ldp + q0,
+                                      sizeof(int32_t) * ldp, 0, sizeof(int32_t) * (q1 - q0),
+                                      r1 - r0, st));
+          g.tail_first = U - R;
+          g.tail_parts = P;
+          g.total_units = U - R + R * P;
+        }
+      }
       CUtensorMap tmb2 = make_slice_map(ctx, slB, kp, n, sb, 128, plane_b, ld);
       OZ_CUDA(launch_gemm_i8_pair(&tma, &tmb2, g, ctx->num_sms, st, &launches));
     } else {

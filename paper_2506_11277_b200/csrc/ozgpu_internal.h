@@ -42,6 +42,10 @@ struct GemmArgs {
   // least that many).  sync = 64 zeroed counters, 128 bytes apart; null = off.
   int* sync;
   int sync_steps, sync_g, sync_d, sync_clusters, sync_prefetch;
+  // split-k tail (CTA-pair kernel): units from tail_first on are the last
+  // partial wave's units, each cut into tail_parts k-ranges whose partial
+  // sums are added into the (pre-zeroed) plane; tail_parts = 0: off
+  int tail_first, tail_parts;
   int32_t* planes;    // [nchunks][m][ldp] int32 chunk sums
   int64_t plane_stride;
   int64_t ldp;

@@ -422,3 +422,26 @@ def test_device_path_graph_replay_is_exact(oz, ref, monkeypatch):
     for _ in range(3):
         got = run()
         assert bits_equal(got, want2), mismatch_report(got, want2)
+
+
+@pytest.mark.parametrize("m,n,k,slices", [(2304, 2050, 700, (9, 8)), (1800, 2600, 512, (7, 7)),
+                                          (3000, 1100, 900, (12, 11)), (8192, 1024, 256, (5, 5))])
+def test_split_k_tail_is_exact(oz, ref, m, n, k, slices, monkeypatch):
+    """The pair GEMM's split-k tail (the last partial wave's units cut into
+    k-ranges whose int32 partial sums are added into pre-zeroed planes)
+    returns exactly the un-split result, and the bottom-right blocks (where
+    the tail tiles sit) match the reference."""
+    rng = np.random.default_rng(m + n + k)
+    a = uniform(m, k, rng)
+    b = random_matrix(k, n, rng, -5, 5, 0.02)
+    cfg = oz.MmaConfig.int8_int32()
+    plan = oz.make_plan(cfg, k, *slices)
+    monkeypatch.setenv("OZGPU_TAIL_SPLIT", "0")
+    want = oz.multiply(a, b, cfg, plan).c
+    monkeypatch.setenv("OZGPU_TAIL_SPLIT", "1")
+    got = oz.multiply(a, b, cfg, plan).c
+    assert bits_equal(got, want), mismatch_report(got, want)
+    blocks = [(m - 8, m, n - 8, n), (m - 300, m - 292, n - 270, n - 262), (0, 8, 0, 8)]
+    exact, _ = ref.ref_multiply_blocks(a, b, slices[0], slices[1], blocks, 3)
+    for r0, r1, c0, c1 in blocks:
+        assert bits_equal(got[r0:r1, c0:c1], exact[r0:r1, c0:c1])
