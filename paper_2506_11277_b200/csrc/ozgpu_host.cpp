@@ -750,7 +750,12 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
         const int clusters = std::min(ctx->num_sms / 2, g.total_units);
         const int U = g.total_units;
         const int R = clusters > 0 ? U % clusters : 0;
-        const int P = R ? clusters / R : 0;
+        // at most 512 (part, chunk) plane tiles of atomic adds (32 M int32
+        // adds): bins of many short chunks (k = 32768) get fewer parts
+        const int nc_last = bfirst.size() >= 2
+                                ? bfirst[bfirst.size() - 1] - bfirst[bfirst.size() - 2]
+                                : 1;
+        const int P = R ? std::min(clusters / R, 512 / (R * std::max(1, nc_last))) : 0;
         if (tail && g.bin_first && R && P >= 2 && pair_tiles >= R && g.kblocks >= P &&
             U >= clusters) {
           const int G = g.group > 0 ? g.group : 8;
