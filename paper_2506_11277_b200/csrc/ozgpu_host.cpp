@@ -20,6 +20,7 @@
 #include <limits>
 #include <memory>
 #include <mutex>
+#include <thread>
 #include <random>
 #include <string>
 #include <vector>
@@ -106,6 +107,25 @@ struct DevBuf {
   }
 };
 
+// Grow-only page-locked host buffer (staging of pageable caller buffers).
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void* get(size_t want) {
+    if (want > bytes) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      bytes = 0;
+      OZ_CUDA(cudaMallocHost(&p, want));
+      bytes = want;
+    }
+    return p;
+  }
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -146,6 +166,8 @@ struct ozgpu_ctx {
   cudaStream_t fork_stream = nullptr;
   cudaEvent_t fork_ev[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> pipe_events;
+  // pinned staging of pageable host A / B / C (ozgpu_dgemm)
+  ozgpu::PinnedBuf stage_a, stage_b, stage_c;
   // stage timing (ozgpu_set_stage_timing)
   bool timing = false;
   std::vector<std::array<cudaEvent_t, 4>> pending_events;
@@ -952,12 +974,81 @@ std::string plan_error(const ozgpu_plan& p) {
 }
 
 // Host-pointer multiply / multiply_axpby.
+void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a,
+                          int64_t lda, const double* b, int64_t ldb, double* c, int64_t ldc,
+                          const ozgpu_mma_config& cfg, const ozgpu_plan& p, ozgpu_diag* diag,
+                          bool axpby, double alpha, double beta, const double* cin,
+                          int64_t ldcin);
+
+bool is_pageable(const void* ptr) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return at.type == cudaMemoryTypeUnregistered;
+}
+
+// rows x cols doubles between strided host buffers, rows split over threads
+void parallel_copy(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
+                   int64_t cols) {
+  if (rows == 0 || cols == 0) return;
+  const int64_t bytes = rows * cols * 8;
+  const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  const int nt = static_cast<int>(std::clamp<int64_t>(bytes >> 24, 1, std::min(hw, 16)));
+  auto work = [&](int t) {
+    const int64_t r0 = rows * t / nt, r1 = rows * (t + 1) / nt;
+    if (ldd == cols && lds == cols) {
+      std::memcpy(dst + r0 * cols, src + r0 * cols, static_cast<size_t>((r1 - r0) * cols * 8));
+    } else {
+      for (int64_t r = r0; r < r1; ++r)
+        std::memcpy(dst + r * ldd, src + r * lds, static_cast<size_t>(cols * 8));
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
+  work(0);
+  for (auto& th : pool) th.join();
+}
+
+// Host-pointer multiply / multiply_axpby.  Pageable caller buffers (the
+// reference's Matrix is a std::vector) copy at ~10 GB/s through the driver's
+// own staging (157 ms vs 36 ms pinned at 8192^3, tools/pageable_probe.py), so
+// large ones are first copied by host threads into the context's pinned
+// buffers (OZGPU_STAGE=0 turns this off; OZGPU_STAGE_MIN = byte threshold).
 void host_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda,
                    const double* b, int64_t ldb, double* c, int64_t ldc,
                    const ozgpu_mma_config& cfg, const ozgpu_plan& p, ozgpu_diag* diag,
                    bool axpby, double alpha, double beta, const double* cin, int64_t ldcin) {
   std::lock_guard<std::mutex> lock(ctx->mu);
   OZ_CUDA(cudaSetDevice(ctx->device));
+  bool stage = !axpby && m > 0 && n > 0 && k > 0;
+  if (const char* env = std::getenv("OZGPU_STAGE")) stage = stage && std::string(env) == "1";
+  int64_t min_bytes = 64 << 20;
+  if (const char* env = std::getenv("OZGPU_STAGE_MIN")) min_bytes = std::atoll(env);
+  stage = stage && 8 * (m * k + k * n + m * n) >= min_bytes &&
+          (is_pageable(a) || is_pageable(b) || is_pageable(c));
+  if (!stage) {
+    host_multiply_locked(ctx, m, n, k, a, lda, b, ldb, c, ldc, cfg, p, diag, axpby, alpha, beta,
+                         cin, ldcin);
+    return;
+  }
+  double* sa = static_cast<double*>(ctx->stage_a.get(sizeof(double) * m * k));
+  double* sb = static_cast<double*>(ctx->stage_b.get(sizeof(double) * k * n));
+  double* sc = static_cast<double*>(ctx->stage_c.get(sizeof(double) * m * n));
+  std::thread tb([&] { parallel_copy(sb, n, b, ldb, k, n); });
+  parallel_copy(sa, k, a, lda, m, k);
+  tb.join();
+  host_multiply_locked(ctx, m, n, k, sa, k, sb, n, sc, n, cfg, p, diag, axpby, alpha, beta, cin,
+                       ldcin);
+  parallel_copy(c, ldc, sc, n, m, n);
+}
+
+void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a,
+                          int64_t lda, const double* b, int64_t ldb, double* c, int64_t ldc,
+                          const ozgpu_mma_config& cfg, const ozgpu_plan& p, ozgpu_diag* diag,
+                          bool axpby, double alpha, double beta, const double* cin,
+                          int64_t ldcin) {
   cudaStream_t st = ctx->stream;
   ValidationResult v = host_validation(cfg, p, k);
   double* da = static_cast<double*>(ctx->in_a.get(sizeof(double) * m * k + 8));

@@ -445,3 +445,26 @@ def test_split_k_tail_is_exact(oz, ref, m, n, k, slices, monkeypatch):
     exact, _ = ref.ref_multiply_blocks(a, b, slices[0], slices[1], blocks, 3)
     for r0, r1, c0, c1 in blocks:
         assert bits_equal(got[r0:r1, c0:c1], exact[r0:r1, c0:c1])
+
+
+@pytest.mark.parametrize("stage_min", ["1", "0"])
+def test_pageable_staging_is_exact(oz, ref, stage_min, monkeypatch):
+    """Pageable host buffers are copied by host threads into the context's
+    pinned buffers before the GPU pipeline (ozgpu_dgemm); the result is
+    bitwise the unstaged one and matches the reference on sampled blocks."""
+    rng = np.random.default_rng(77)
+    m, k, n = 1100, 900, 1300
+    a = uniform(m, k, rng)
+    b = random_matrix(k, n, rng, -9, 9, 0.02)
+    cfg = oz.MmaConfig.int8_int32()
+    plan = oz.make_plan(cfg, k, 8, 7)
+    monkeypatch.setenv("OZGPU_STAGE", "0")
+    want = oz.multiply(a, b, cfg, plan).c
+    monkeypatch.setenv("OZGPU_STAGE", "1")
+    monkeypatch.setenv("OZGPU_STAGE_MIN", stage_min)
+    got = oz.multiply(a, b, cfg, plan).c
+    assert bits_equal(got, want), mismatch_report(got, want)
+    blocks = [(0, 8, 0, 8), (m - 8, m, n - 8, n)]
+    exact, _ = ref.ref_multiply_blocks(a, b, 8, 7, blocks, 2)
+    for r0, r1, c0, c1 in blocks:
+        assert bits_equal(got[r0:r1, c0:c1], exact[r0:r1, c0:c1])
