@@ -7,26 +7,39 @@ Metric (BASELINE.json): effective FP64-equivalent TFLOP/s = 2mnk / t, with
 the int8 tensor-pipe rate of the pair GEMMs (2*chi*mnk / t_gemm) reported
 against the int8 dense peak as the roofline.
 
-Workload at N=1: configs[1] -- FP64 GEMM m=n=k=8192, uniform(-0.5, 0.5) inputs
-from the reference generator (seeds 1 and 2), slice counts chosen by the
-reference's estimator for a 1e-15 target (SURVEY.md 8d) -> (12, 12), chi=78;
-the s=3..8 sweep of the same config is reported beside it.
+Workload at N=1 (default): configs[1] -- FP64 GEMM m=n=k=8192, uniform(-0.5,
+0.5) inputs from the reference generator (seeds 1 and 2), slice counts chosen
+by the reference's estimator for a 1e-15 target -> (12, 12),
+chi=78; the s=3..8 sweep of the same config and a north-star sub-record
+(16384^3, estimator (13, 12)) are reported beside it.
 
-N > 1 (torchrun, one process per GPU, NCCL): weak scaling with 2-D C tiles --
-rank (i, j) computes an m x n block of a (p_r m) x (p_c n) product with the
-full k; A row-panel i lives on rank (i, 0) and B column-panel j on (0, j) and
-is broadcast along its row / column group each step (the only exchange step).
+N > 1 (default configs[4]): strong scaling of the 32768^3 product over 2-D C
+tiles, one process per GPU over NCCL.  Rank (i, j) computes its C block with
+the full k; A row-panel i exists only on rank (i, 0) and B column-panel j only
+on rank (0, j) and is broadcast along its row / column group every step (the
+only exchange; scales are per row / column so blocks are independent).
+Without WORLD_SIZE in the environment, `--gpus N` re-launches itself under
+torch.distributed.run with N ranks.  A weak-scaling sub-record (an 8192^3
+block per rank) rides along.
 
 A "step" = one multiply (slicing + pair GEMMs + exact combine) with inputs
 resident in HBM; `e2e` = the same through the host-pointer C-ABI call
-(H2D of A and B, D2H of C inside the timed region).  Inputs (512 MiB each at
-8192^2) exceed the 126 MB L2, so no explicit flush is needed.
+(H2D of A and B, D2H of C inside the timed region, pinned buffers;
+`e2e_pageable` from plain pageable arrays).  Inputs (512 MiB each at 8192^2)
+exceed the 126 MB L2, so no explicit flush is needed.
+
+`--impl reference` runs the reference's own multiply() (oracle/_ref, compiled
+from the unmodified reference sources) on sampled C blocks on all host
+cores, with inputs from the reference's generators and slices from the
+reference's estimator -- nothing from this repository's package is imported.
 """
 from __future__ import annotations
 
 import argparse
+import importlib.util
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -60,70 +73,178 @@ CONFIGS = {
 METRIC = "effective FP64-equiv TFLOP/s (2mnk/t) and int8 tensor-pipe % of peak vs slices"
 
 
-def _peaks():
-    """(int8 dense peak TOPS, its sustained twin, HBM GB/s, how) from the
-    driver-measured bf16 cuBLAS rates (sm_100 int8 dense = 2x bf16 per clock)."""
-    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    try:
-        with open(path) as f:
-            mp = json.load(f)
-        bf16 = float(mp["bf16_tflops"])
-        sus = float(mp.get("bf16_tflops_sustained", bf16))
-        return 2.0 * bf16, 2.0 * sus, float(mp.get("hbm_gbs", 6535.4)), \
-            f"peak = 2 x measured bf16 cuBLAS burst ({bf16} TFLOP/s, MEASURED_PEAKS.json; " \
-            f"the conservative choice); peak_sustained = 2 x the sustained bf16 rate ({sus}), " \
-            f"the figure for a kernel timed inside a long step.  Unthrottled tcgen05 " \
-            f"kind::i8 issue ceiling measured with tools/ubench/mma_rate.cu: 128 cycles per " \
-            f"128x256x32 MMA (4.6 POPS at 1965 MHz)"
-    except Exception:
-        return 2.0 * 1590.0, 2.0 * 1590.0, 6650.0, \
-            "2 x fallback bf16 1.59 PFLOP/s (B200_PROFILING.md)"
+def _load_shard():
+    """paper_2506_11277_b200/shard.py as a standalone module (pure Python; the
+    package itself, which loads the CUDA library, is not imported)."""
+    path = os.path.join(ROOT, "paper_2506_11277_b200", "shard.py")
+    spec = importlib.util.spec_from_file_location("_oz_shard", path)
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[spec.name] = mod
+    spec.loader.exec_module(mod)
+    return mod
 
 
-def _traffic(workload: str):
-    path = os.path.join(ROOT, "profiles", "ncu_gemm_traffic.json")
-    try:
-        with open(path) as f:
-            return json.load(f).get(workload)
-    except Exception:
-        return None
+shard = _load_shard()
+
+
+# ------------------------------------------------------------ plan facts
+# (host arithmetic shared by both arms so their config records are identical)
+
+def ceil_log2(x: int) -> int:
+    return (x - 1).bit_length()
+
+
+def slice_width(k: int) -> int:
+    """optimal_slice_width (mma_sim.cpp:50-59) for MmaConfig::int8_int32()."""
+    return min(7, (31 - ceil_log2(k)) // 2)
+
+
+def chi_of(sa: int, sb: int) -> int:
+    """chi (scheme.cpp:46-52), the reduced schedule's pair count."""
+    lo, hi = min(sa, sb), max(sa, sb)
+    return lo * (2 * hi - lo + 1) // 2
 
 
 def chunk_count(sa, sb, k, t):
     """Chunk planes of the levelled-exact plan (reduced schedule): each
     diagonal's pairs in runs whose int32 sum cannot overflow (build_chunks)."""
     cap = max(1, (2**31 - 1) // (k * (2**t - 1) ** 2))
-    dmax = max(sa, sb)
     total = 0
-    for d in range(dmax):
+    for d in range(max(sa, sb)):
         lo, hi = max(1, d + 2 - sb), min(sa, d + 1)
-        w = max(0, hi - lo + 1)
-        total += -(-w // cap)
+        total += -(-max(0, hi - lo + 1) // cap)
     return total
 
 
-def make_inputs(oz, cfg, rank_i=0, rank_j=0):
-    m, n, k = cfg["m"], cfg["n"], cfg["k"]
-    if cfg["gen"] == "uniform":
-        a = oz.random_uniform(m, k, 1 + 1000 * rank_i, -0.5, 0.5)
-        b = oz.random_uniform(k, n, 2 + 1000 * rank_j, -0.5, 0.5)
+def sample_block(k: int) -> int:
+    """Edge of the sampled C blocks the CPU legs time (one block per core): a
+    block costs ~b^2 k chi int8 MACs on the reference's scalar loop, so b
+    shrinks with k to keep one sample step at a few seconds."""
+    return 64 if k <= 2048 else 32 if k <= 8192 else 16
+
+
+def cpu_blocks(m, n, count, bs):
+    """Deterministic spread of `count` bs x bs C blocks."""
+    out = []
+    nbr, nbc = max(1, m // bs), max(1, n // bs)
+    for t in range(count):
+        bi = (t * 7919 + 3) % nbr
+        bj = (t * 104729 + 5) % nbc
+        out.append((bi * bs, min(m, bi * bs + bs), bj * bs, min(n, bj * bs + bs)))
+    return out
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def geometry(cfg, world, rank):
+    """(block, m, n, global_m, global_n): strong scaling splits the configured
+    product; weak scaling gives every rank a full configured-size block."""
+    pr, pc = shard.grid_for(world)
+    if cfg.get("strong"):
+        gm, gn = cfg["m"], cfg["n"]
     else:
-        a, b = oz.gen_kappa_d(k, 2.0 ** 60, 7 + 1000 * (rank_i + rank_j), True)
-    return a, b
+        gm, gn = pr * cfg["m"], pc * cfg["n"]
+    blk = shard.block_of(rank, world, gm, gn)
+    return blk, blk.row1 - blk.row0, blk.col1 - blk.col0, gm, gn
 
 
-def choose_slices(oz, cfg, a, b):
-    if cfg["slices"] != "estimator":
-        return tuple(cfg["slices"]), None
-    mcfg = oz.MmaConfig.int8_int32()
-    t = oz.optimal_slice_width(mcfg, cfg["k"])
-    prof = oz.scaling_profile(a, b)
-    acc_bits = 2 * t + (cfg["k"] - 1).bit_length()
-    sel = oz.select_slices(prof.kappa_a, prof.kappa_b, t, U53, 24,
-                           oz.SelectOptions(target=1e-15, acc_bits_used=acc_bits))
-    return (sel.slices_a, sel.slices_b), {"kappa_a": prof.kappa_a, "kappa_b": prof.kappa_b,
-                                          "target": 1e-15, "lhs": sel.lhs}
+def config_record(cfg, world, m, n, gm, gn, slices):
+    k = cfg["k"]
+    pr, pc = shard.grid_for(world)
+    return {"workload": cfg["name"], "m": m, "n": n, "k": k, "global_m": gm, "global_n": gn,
+            "grid": [pr, pc], "slices": list(slices), "chi": chi_of(*slices),
+            "width": slice_width(k), "schedule": "reduced", "strategy": "levelled-exact",
+            "l2": "inputs larger than L2 (A = %d MiB > 126 MB)" % (8 * m * k // 2**20)
+                  if 8 * m * k > 126e6 else "A = %d MiB: operands fit the 126 MB L2 (no flush; launch-bound config)" %
+                  (8 * m * k // 2**20),
+            "parallelism": f"2-D C tiles {pr}x{pc}"}
 
+
+def data_note(cfg):
+    if cfg["gen"] == "uniform":
+        return ("synthetic: reference generator random_uniform(-0.5,0.5), A row-panel i seed "
+                "1+1000i, B column-panel j seed 2+1000j (seeds 1, 2 at N=1)")
+    return "synthetic: reference gen_kappa_d(2^60, seed 7, rotate)"
+
+
+def panel_seeds(i, j):
+    return 1 + 1000 * i, 2 + 1000 * j
+
+
+# ------------------------------------------------------------ reference arm
+
+def reference_arm(args, cfg_key):
+    """The reference's own CPU path: oracle/_ref is the unmodified reference
+    compiled from its sources; inputs from its generators, slices from its
+    estimator (scaling_profile + select_slices); nothing from the product."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    from oracle import pyoracle as po
+    cfg = CONFIGS[cfg_key]
+    blk, m, n, gm, gn = geometry(cfg, world, 0)
+    k = cfg["k"]
+    line = {"metric": METRIC, "unit": "TFLOP/s", "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "strong" if cfg.get("strong") else "weak", "vs_baseline": None,
+            "dtype": "int8", "data": data_note(cfg)}
+    if not po.have_ref():
+        line["unavailable"] = "oracle/_ref/libozref.so not built"
+        print(json.dumps(line))
+        return
+    if cfg["gen"] == "uniform":
+        sa_, sb_ = panel_seeds(blk.i, blk.j)
+        a = po.ref_random_uniform(m, k, sa_, -0.5, 0.5)
+        b = po.ref_random_uniform(k, n, sb_, -0.5, 0.5)
+    else:
+        a, b = po.ref_gen_kappa_d(k, 2.0 ** 60, 7, True)
+    t = slice_width(k)
+    if cfg["slices"] == "estimator":
+        ka, kb, _, _ = po.ref_scaling_profile(a, b)
+        sel = po.ref_select_slices(ka, kb, t, U53, 24, target=1e-15,
+                                   acc_bits_used=2 * t + ceil_log2(k))
+        slices = (sel["slices_a"], sel["slices_b"])
+        est = {"kappa_a": ka, "kappa_b": kb, "target": 1e-15, "lhs": sel["lhs"],
+               "via": "reference scaling_profile + select_slices (analysis.cpp:58-68,142-207)"}
+    else:
+        slices, est = tuple(cfg["slices"]), None
+    threads = os.cpu_count() or 1
+    bs = sample_block(k)
+    blocks = cpu_blocks(m, n, threads, bs)
+    rates, walls = [], []
+    for s in range(args.warmup + args.steps):
+        _, secs = po.ref_multiply_blocks(a, b, slices[0], slices[1], blocks, threads)
+        flops = sum(2.0 * (r1 - r0) * (c1 - c0) * k for r0, r1, c0, c1 in blocks)
+        if s >= args.warmup:
+            rates.append(flops / secs / 1e12)
+            walls.append(secs)
+    value = statistics.mean(rates)
+    sample = (f"{len(blocks)} C blocks of {bs}x{bs} with full k={k} per step (one per host "
+              f"thread), reference multiply() (oracle/_ref, compiled from the reference "
+              f"sources) on {threads} threads of {cpu_model()}; rate = sampled FP64-equiv "
+              f"flops / wall time (extrapolates to the full product: blocking is exact)")
+    line.update({"value": value, "ms_per_step": 1e3 * statistics.mean(walls),
+                 "config": config_record(cfg, world, m, n, gm, gn, slices),
+                 "estimator": est,
+                 "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads,
+                                  "kind": "reference", "sample": sample,
+                                  "cpu_model": cpu_model(), "nproc": os.cpu_count()},
+                 "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                         "d2h_bytes_per_step": 0}})
+    print(json.dumps(line))
+
+
+# ------------------------------------------------------------ measurement helpers
 
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
@@ -184,102 +305,122 @@ def bad_clocks(c) -> bool:
     return False
 
 
-def cpu_blocks(m, n, count, bs):
-    """Deterministic spread of `count` bs x bs C blocks."""
-    out = []
-    nbr, nbc = max(1, m // bs), max(1, n // bs)
-    for t in range(count):
-        bi = (t * 7919 + 3) % nbr
-        bj = (t * 104729 + 5) % nbc
-        out.append((bi * bs, min(m, bi * bs + bs), bj * bs, min(n, bj * bs + bs)))
-    return out
-
-
-def run_cpu_reference(a, b, slices, blocks, threads):
-    """Reference multiply() (oracle/_ref) over sampled C blocks -> (C, seconds)."""
-    from oracle import pyoracle
-    return pyoracle.ref_multiply_blocks(a, b, slices[0], slices[1], blocks, threads)
-
-
-def reference_arm(args, cfg_key):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
-    import paper_2506_11277_b200 as oz  # host-side generator + estimator only
-    from oracle import pyoracle
-    cfg = CONFIGS[cfg_key]
-    line = {"metric": METRIC, "unit": "TFLOP/s", "impl": "reference", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int8",
-            "data": "synthetic: reference generator random_uniform(-0.5,0.5) seeds 1,2"
-                    if cfg["gen"] == "uniform" else
-                    "synthetic: reference gen_kappa_d(2^60, seed 7, rotate)",
-            "config": {"workload": cfg["name"], "m": cfg["m"], "n": cfg["n"], "k": cfg["k"]}}
-    if not pyoracle.have_ref():
-        line["unavailable"] = "oracle/_ref/libozref.so not built"
-        print(json.dumps(line))
-        return
-    a, b = make_inputs(oz, cfg)
+def _peaks():
+    """(int8 dense peak, its sustained twin, HBM GB/s, how) from the
+    driver-measured bf16 cuBLAS rates (sm_100 int8 dense = 2x bf16 per clock)."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
-        slices, est = choose_slices(oz, cfg, a, b)
+        with open(path) as f:
+            mp = json.load(f)
+        bf16 = float(mp["bf16_tflops"])
+        sus = float(mp.get("bf16_tflops_sustained", bf16))
+        return 2.0 * bf16, 2.0 * sus, float(mp.get("hbm_gbs", 6548.2)), \
+            f"peak = 2 x measured bf16 cuBLAS burst ({bf16} TFLOP/s, MEASURED_PEAKS.json): the " \
+            f"recipe's figure for a kernel timed inside a short step; frac_sustained uses " \
+            f"2 x the sustained bf16 rate ({sus}).  Unthrottled tcgen05 kind::i8 issue " \
+            f"ceiling measured with tools/ubench/mma_rate.cu: 128 cycles per 128x256x32 MMA " \
+            f"(4.6 POPS at 1965 MHz)"
     except Exception:
-        # no GPU for the estimator's kappa scan: run the reference estimator
-        ka, kb, _, _ = pyoracle.ref_scaling_profile(a, b)
-        t = 7
-        acc = 2 * t + (cfg["k"] - 1).bit_length()
-        sel = pyoracle.ref_select_slices(ka, kb, t, U53, 24, target=1e-15, acc_bits_used=acc)
-        slices, est = (sel["slices_a"], sel["slices_b"]), {"kappa_a": ka, "kappa_b": kb}
-    if cfg["slices"] != "estimator":
-        slices = tuple(cfg["slices"])
-    threads = os.cpu_count() or 1
-    bs = 32 if cfg["k"] >= 4096 else 64
-    if cfg["m"] * cfg["n"] <= 1024 * 1024 and cfg["k"] <= 1024:
-        bs = 64
-    blocks = cpu_blocks(cfg["m"], cfg["n"], threads, bs)
-    rates, walls = [], []
-    for s in range(args.warmup + args.steps):
-        _, secs = run_cpu_reference(a, b, slices, blocks, threads)
-        flops = sum(2.0 * (r1 - r0) * (c1 - c0) * cfg["k"] for r0, r1, c0, c1 in blocks)
-        if s >= args.warmup:
-            rates.append(flops / secs / 1e12)
-            walls.append(secs)
-    value = statistics.mean(rates)
-    sample = (f"{len(blocks)} C blocks of {bs}x{bs} with full k={cfg['k']} per step, reference "
-              f"multiply() (oracle/_ref, compiled from the reference sources) on {threads} "
-              f"host threads; rate = sampled FP64-equiv flops / wall time")
-    line.update({"value": value, "ms_per_step": 1e3 * statistics.mean(walls),
-                 "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads,
-                                  "kind": "reference", "sample": sample},
-                 "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
-                         "d2h_bytes_per_step": 0}})
-    line["config"].update({"slices": list(slices), "chi": oz.chi(*slices)})
-    print(json.dumps(line))
+        return 2.0 * 1590.0, 2.0 * 1590.0, 6650.0, \
+            "2 x fallback bf16 1.59 PFLOP/s (B200_PROFILING.md)"
 
+
+def _committed_traffic(cfg_key):
+    path = os.path.join(ROOT, "profiles", "ncu_gemm_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(cfg_key)
+    except Exception:
+        return None
+
+
+def measure_traffic(cfg_key, timeout=300):
+    """DRAM bytes of one pair-GEMM launch, measured now: this script re-run
+    under ncu (dram__bytes_read.sum + dram__bytes_write.sum of the 2nd
+    gemm_i8 launch, --clock-control none).  Nothing from that child run is
+    used but the counter."""
+    log = os.path.join(ROOT, "gpurun_out", f"traffic_{cfg_key}_{os.getpid()}.csv")
+    os.makedirs(os.path.dirname(log), exist_ok=True)
+    cmd = ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+           "--clock-control", "none", "--print-units", "base", "-k", "regex:gemm_i8", "-s", "1",
+           "-c", "1", "--csv", "--log-file", log, sys.executable, os.path.abspath(__file__),
+           "--config", cfg_key, "--steps", "1", "--warmup", "3", "--no-e2e", "--no-cpu-baseline",
+           "--no-sweep", "--no-traffic", "--no-north-star"]
+    env = dict(os.environ, OZGPU_GRAPH="0")
+    try:
+        subprocess.run(cmd, env=env, timeout=timeout, stdout=subprocess.DEVNULL,
+                       stderr=subprocess.DEVNULL, cwd=ROOT)
+        import csv
+        vals, kernel = {}, None
+        with open(log) as f:
+            rows = [r for r in csv.reader(l for l in f if l.startswith('"'))]
+        head = rows[0]
+        for r in rows[1:]:
+            rec = dict(zip(head, r))
+            vals[rec["Metric Name"]] = float(rec["Metric Value"].replace(",", ""))
+            kernel = rec.get("Kernel Name")
+        return {"bytes": vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"],
+                "read": vals["dram__bytes_read.sum"], "write": vals["dram__bytes_write.sum"],
+                "ncu_ns": vals.get("gpu__time_duration.sum"), "kernel": kernel,
+                "source": "measured in this run (ncu child, one launch)"}
+    except Exception as e:  # context only: never fail the bench line
+        c = _committed_traffic(cfg_key)
+        return {"bytes": c, "source": f"profiles/ncu_gemm_traffic.json (measurement failed: "
+                                      f"{type(e).__name__})"} if c else None
+    finally:
+        try:
+            os.remove(log)
+        except OSError:
+            pass
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+# ------------------------------------------------------------ our arm
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                    help="default: c2 (configs[1]) at N=1, c5 (configs[4], strong) at N>1")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-traffic", action="store_true")
+    ap.add_argument("--no-north-star", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    env_world = os.environ.get("WORLD_SIZE")
+    if args.config is None:
+        args.config = "c2" if int(env_world or args.gpus) == 1 else "c5"
     if args.impl == "reference":
         reference_arm(args, args.config)
         return
+    if env_world is None and args.gpus > 1:
+        # one process per GPU: re-launch under torch.distributed.run
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd, env=dict(os.environ)))
+    world = int(env_world or "1")
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines (nranks) in the log
 
     import numpy as np
     import torch
     import torch.distributed as dist
 
     import paper_2506_11277_b200 as oz
-    from paper_2506_11277_b200 import shard
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -287,46 +428,72 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     cfg = dict(CONFIGS[args.config])
-    m, n, k = cfg["m"], cfg["n"], cfg["k"]
-    pr, pc = shard.grid_for(world)
-    strong = bool(cfg.get("strong"))
-    if strong:
-        # a fixed global m x n split into the ranks' C blocks
-        blk = shard.block_of(rank, world, m, n)
-        gm, gn = m, n
-        m, n = blk.row1 - blk.row0, blk.col1 - blk.col0
-        cfg["m"], cfg["n"] = m, n
-    else:
-        # weak scaling: every rank a full m x n block of a (p_r m) x (p_c n) product
-        blk = shard.block_of(rank, world, pr * m, pc * n)
-        gm, gn = pr * m, pc * n
+    k = cfg["k"]
+    blk, m, n, gm, gn = geometry(cfg, world, rank)
     mcfg = oz.MmaConfig.int8_int32()
     dev = torch.device(f"cuda:{local}")
     # a dedicated stream: CUDA events and the library's kernels share it
     torch.cuda.set_stream(torch.cuda.Stream(device=dev))
-
-    # inputs: A row-panel i on rank (i, 0), B column-panel j on rank (0, j)
-    a_h, b_h = make_inputs(oz, cfg, blk.i, blk.j)
-    slices, est = choose_slices(oz, cfg, a_h, b_h)
-    if world > 1:  # one plan for the whole job: the max over ranks
-        t = torch.tensor(list(slices), device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        slices = tuple(int(v) for v in t.tolist())
-    plan = oz.make_plan(mcfg, k, slices[0], slices[1])
-    chi = oz.chi(*slices)
-    a_d = torch.from_numpy(a_h).to(dev)
-    b_d = torch.from_numpy(b_h).to(dev)
-    c_d = torch.empty((m, n), dtype=torch.float64, device=dev)
-    status = torch.zeros(1, dtype=torch.int32, device=dev)
     xchg = shard.PanelExchange(world, rank)
 
-    def step(p=plan):
-        xchg.exchange(a_d, b_d)  # A row-panel / B column-panel from their owners (NCCL)
-        oz.multiply_device(m, n, k, a_d.data_ptr(), k, b_d.data_ptr(), n, c_d.data_ptr(), n,
-                           mcfg, p, stream=torch.cuda.current_stream().cuda_stream,
-                           status_ptr=status.data_ptr())
+    def load_panels(cfg_):
+        """A row-panel i exists only on rank (i, 0), B column-panel j only on
+        (0, j); the others receive them in the exchange."""
+        blk_, m_, n_, _, _ = geometry(cfg_, world, rank)
+        k_ = cfg_["k"]
+        a_d = torch.zeros((m_, k_), dtype=torch.float64, device=dev)
+        b_d = torch.zeros((k_, n_), dtype=torch.float64, device=dev)
+        if cfg_["gen"] == "uniform":
+            sa_, sb_ = panel_seeds(blk_.i, blk_.j)
+            if rank == shard.a_owner(world, blk_.i):
+                a_d.copy_(torch.from_numpy(oz.random_uniform(m_, k_, sa_, -0.5, 0.5)))
+            if rank == shard.b_owner(world, blk_.j):
+                b_d.copy_(torch.from_numpy(oz.random_uniform(k_, n_, sb_, -0.5, 0.5)))
+        else:
+            a_h, b_h = oz.gen_kappa_d(k_, 2.0 ** 60, 7, True)
+            a_d.copy_(torch.from_numpy(a_h))
+            b_d.copy_(torch.from_numpy(b_h))
+        xchg.exchange(a_d, b_d)
+        torch.cuda.synchronize()
+        return a_d, b_d, m_, n_
 
-    def timed(nsteps, p=plan):
+    def estimate(cfg_, a_h, b_h):
+        if cfg_["slices"] != "estimator":
+            return tuple(cfg_["slices"]), None
+        t = oz.optimal_slice_width(mcfg, cfg_["k"])
+        prof = oz.scaling_profile(a_h, b_h)  # the GPU kappa scan
+        sel = oz.select_slices(prof.kappa_a, prof.kappa_b, t, U53, 24,
+                               oz.SelectOptions(target=1e-15,
+                                                acc_bits_used=2 * t + ceil_log2(cfg_["k"])))
+        sl = (sel.slices_a, sel.slices_b)
+        if world > 1:  # one plan for the whole job: the max over ranks
+            tt = torch.tensor(list(sl), device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            sl = tuple(int(v) for v in tt.tolist())
+        return sl, {"kappa_a": prof.kappa_a, "kappa_b": prof.kappa_b, "target": 1e-15,
+                    "lhs": sel.lhs, "via": "GPU kappa scan + host select_slices"}
+
+    a_d, b_d, m, n = load_panels(cfg)
+    a_h, b_h = a_d.cpu().numpy(), b_d.cpu().numpy()
+    slices, est = estimate(cfg, a_h, b_h)
+    plan = oz.make_plan(mcfg, k, slices[0], slices[1])
+    chi = oz.chi(*slices)
+    c_d = torch.empty((m, n), dtype=torch.float64, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def make_step(a_, b_, c_, m_, n_, k_, exchange=True):
+        def step(p):
+            if exchange:
+                xchg.exchange(a_, b_)  # panels from their owners (NCCL broadcast)
+            oz.multiply_device(m_, n_, k_, a_.data_ptr(), k_, b_.data_ptr(), n_, c_.data_ptr(), n_,
+                               mcfg, p, stream=torch.cuda.current_stream().cuda_stream,
+                               status_ptr=status.data_ptr())
+        return step
+
+    step = make_step(a_d, b_d, c_d, m, n, k)
+
+    def timed(nsteps, p, stepf=None):
+        stepf = stepf or step
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -336,20 +503,20 @@ def main():
         l0 = oz.kernel_launches()
         e0.record(stream)
         for _ in range(nsteps):
-            step(p)
+            stepf(p)
         e1.record(stream)
         torch.cuda.synchronize()
         launches = oz.kernel_launches() - l0
         ms = e0.elapsed_time(e1) / nsteps
         if world > 1:
-            t = torch.tensor([ms], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
+            tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt.item())
             dist.barrier()
         return ms, launches
 
     for _ in range(args.warmup):
-        step()
+        step(plan)
     torch.cuda.synchronize()
     if int(status.item()) != 0:
         raise RuntimeError("multiply: inputs must be finite with no negative zeros")
@@ -360,77 +527,81 @@ def main():
     attempt = 0
     while True:
         sampler.start()
-        ms, launches = timed(args.steps)
+        ms, launches = timed(args.steps, plan)
         clocks = sampler.stop()
         attempt += 1
         if not bad_clocks(clocks) or attempt >= 2:
             break
     if attempt == 2:
         clocks["remeasured"] = True
-    # stage breakdown (CUDA events between the stages; eager launches)
-    oz.stage_times(reset=True)
-    oz.set_stage_timing(True)
-    timed(args.steps)  # as long as the headline loop: the same power-capped clock
-    oz.set_stage_timing(False)
-    slice_ms, gemm_ms, comb_ms, calls = oz.stage_times(reset=True)
+
+    def stage_split(nsteps, p, stepf=None):
+        """Stage times from an eager loop of the same length (CUDA events
+        between the stages, on the launching stream)."""
+        oz.stage_times(reset=True)
+        oz.set_stage_timing(True)
+        timed(nsteps, p, stepf)
+        oz.set_stage_timing(False)
+        s_ms, g_ms, c_ms, calls = oz.stage_times(reset=True)
+        calls = max(calls, 1)
+        return s_ms / calls, g_ms / calls, c_ms / calls
+
+    slice_ms, gemm_ms, comb_ms = stage_split(args.steps, plan)
+    peak, peak_sus, hbm_peak, peak_how = _peaks()
+
+    def rooflines(m_, n_, k_, sl, g_ms, s_ms, c_ms):
+        ch = chi_of(*sl)
+        tops = 2.0 * ch * m_ * n_ * k_ / (g_ms * 1e-3) / 1e12
+        sbytes = 8.0 * (m_ * k_ + k_ * n_) + sl[0] * m_ * k_ + sl[1] * k_ * n_ + 4.0 * (m_ + n_)
+        nch = chunk_count(sl[0], sl[1], k_, slice_width(k_))
+        cbytes = 4.0 * nch * m_ * n_ + 8.0 * m_ * n_ + 4.0 * (m_ + n_)
+        return tops, {
+            "roofline": {"bound": "tensor", "achieved": tops, "peak": peak, "unit": "TFLOP/s",
+                         "frac": tops / peak, "traffic": None,
+                         "peak_kind": "measured: 2 x bf16 cuBLAS burst (MEASURED_PEAKS.json)",
+                         "frac_sustained": tops / peak_sus, "peak_sustained": peak_sus,
+                         "kernel": "gemm_i8_pair_kernel<6> (tcgen05.mma.cta_group::2.kind::i8, "
+                                   "256x256 tiles, equal-length chunk bins, wave lockstep)",
+                         "algorithmic": "2*chi*m*n*k int8 ops per launch (%.4g)" %
+                                        (2.0 * ch * m_ * n_ * k_),
+                         "launch_ms": g_ms, "peak_note": peak_how},
+            "slicing_roofline": {"bound": "hbm", "achieved": sbytes / (s_ms * 1e-3) / 1e9,
+                                 "peak": hbm_peak, "unit": "GB/s",
+                                 "frac": sbytes / (s_ms * 1e-3) / 1e9 / hbm_peak,
+                                 "algorithmic": "8(mk+kn) + s_A mk + s_B kn + 4(m+n) bytes "
+                                                "(%.4g)" % sbytes, "ms": s_ms},
+            "combine_roofline": {"bound": "hbm", "achieved": cbytes / (c_ms * 1e-3) / 1e9,
+                                 "peak": hbm_peak, "unit": "GB/s",
+                                 "frac": cbytes / (c_ms * 1e-3) / 1e9 / hbm_peak,
+                                 "algorithmic": "4 * chunks * m * n (int32 chunk planes) + 8 m n "
+                                                "(C) bytes (%.4g)" % cbytes,
+                                 "chunks": nch, "ms": c_ms}}
 
     flops_rank = 2.0 * m * n * k  # this rank's block
     flops_total = 2.0 * gm * gn * k  # the whole job (all ranks' blocks)
     value = flops_total / (ms * 1e-3) / 1e12
-    gemm_ms_call = gemm_ms / max(calls, 1)
-    int8_ops = 2.0 * chi * m * n * k
-    tops = int8_ops / (gemm_ms_call * 1e-3) / 1e12
-    peak, peak_sus, hbm_peak, peak_how = _peaks()
-    # the driver's rule: the burst peak for a kernel timed alone, the
-    # sustained (power-capped) one for a kernel timed inside a long step
-    long_region = ms * args.steps >= 500.0
-    peak_used = peak_sus if long_region else peak
-    peak_kind = ("of measured: 2 x bf16 cuBLAS sustained (timed region %.0f ms >= 500 ms)" if
-                 long_region else "of measured: 2 x bf16 cuBLAS burst (timed region %.0f ms)") % \
-        (ms * args.steps)
-    slice_bytes = 8.0 * (m * k + k * n) + slices[0] * m * k + slices[1] * k * n + 4.0 * (m + n)
-    nch = chunk_count(slices[0], slices[1], k, plan.width)
-    comb_bytes = 4.0 * nch * m * n + 8.0 * m * n + 4.0 * (m + n)
-    slice_ms_call = slice_ms / max(calls, 1)
+    tops, roofs = rooflines(m, n, k, slices, gemm_ms, slice_ms, comb_ms)
 
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
-        "dtype": "int8",
-        "data": "synthetic: reference generator random_uniform(-0.5,0.5) seeds 1,2 "
-                "(per-panel seeds 1+1000i / 2+1000j for N>1)" if cfg["gen"] == "uniform" else
-                "synthetic: reference gen_kappa_d(2^60, seed 7, rotate)",
-        "config": {"workload": cfg["name"], "m": m, "n": n, "k": k,
-                   "global_m": gm, "global_n": gn, "grid": [pr, pc],
-                   "slices": list(slices), "chi": chi, "width": plan.width,
-                   "schedule": "reduced", "strategy": "levelled-exact", "estimator": est,
-                   "launch": "CUDA-graph replay of the whole multiply (captured on the 2nd call); "
-                             "stage_ms / int8_tops from a second loop of the same length, eager, "
-                             "with CUDA events between the stages",
-                   "l2": "inputs larger than L2 (A, B = %d MiB each > 126 MB)" %
-                         (8 * m * k // 2**20), "parallelism": f"2-D C tiles {pr}x{pc}"},
+        "higher_is_better": True, "scaling": "strong" if cfg.get("strong") else "weak",
+        "vs_baseline": None, "dtype": "int8", "data": data_note(cfg),
+        "config": config_record(cfg, world, m, n, gm, gn, slices),
+        "estimator": est,
+        "launch": "headline: CUDA-graph replay of the whole multiply (captured on the 2nd call); "
+                  "stage_ms / int8_tops from a second loop of the same length, eager, with "
+                  "CUDA events between the stages",
         "int8_tops": tops,
-        "stage_ms": {"slicing": slice_ms_call, "pair_gemms": gemm_ms_call,
-                     "combine": comb_ms / max(calls, 1)},
-        "roofline": {"bound": "tensor", "achieved": tops, "peak": peak_used, "unit": "TFLOP/s",
-                     "frac": tops / peak_used, "traffic": _traffic(args.config),
-                     "peak_kind": peak_kind, "peak_burst": peak, "peak_sustained": peak_sus,
-                     "kernel": "gemm_i8_pair_kernel<6> (tcgen05.mma.cta_group::2.kind::i8, "
-                               "256x256 tiles, equal-length chunk bins, wave lockstep)",
-                     "algorithmic": "2*chi*m*n*k int8 ops per launch", "peak_note": peak_how},
-        "slicing_roofline": {"bound": "hbm", "achieved": slice_bytes / (slice_ms_call * 1e-3) / 1e9,
-                             "peak": hbm_peak, "unit": "GB/s",
-                             "frac": slice_bytes / (slice_ms_call * 1e-3) / 1e9 / hbm_peak,
-                             "algorithmic": "8(mk+kn) + s_A mk + s_B kn + 4(m+n) bytes"},
-        "combine_roofline": {"bound": "hbm", "achieved": comb_bytes / (comb_ms / max(calls, 1) * 1e-3) / 1e9,
-                             "peak": hbm_peak, "unit": "GB/s",
-                             "frac": comb_bytes / (comb_ms / max(calls, 1) * 1e-3) / 1e9 / hbm_peak,
-                             "algorithmic": "4 * chunks * m * n (int32 chunk planes) + 8 m n (C) bytes",
-                             "chunks": nch},
+        "stage_ms": {"slicing": slice_ms, "pair_gemms": gemm_ms, "combine": comb_ms},
+        **roofs,
         "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
         "clocks": clocks,
     }
+    if world > 1:
+        line["exchange"] = ("A row-panel (%d x %d) broadcast along row groups, B column-panel "
+                            "(%d x %d) along column groups (NCCL), inside every timed step" %
+                            (m, k, k, n))
 
     # s = 3..8 sweep of configs[1] (same inputs), fewer steps each
     if cfg.get("sweep") and not args.no_sweep:
@@ -439,14 +610,11 @@ def main():
             ps = oz.make_plan(mcfg, k, s, s)
             for _ in range(2):
                 step(ps)
-            oz.stage_times(reset=True)
-            oz.set_stage_timing(True)
             sms, _ = timed(max(3, args.steps // 4), ps)
-            oz.set_stage_timing(False)
-            _, g_ms, _, c_ = oz.stage_times(reset=True)
+            _, g_ms, _ = stage_split(max(3, args.steps // 4), ps)
             ch = oz.chi(s, s)
             sweep.append({"s": s, "chi": ch, "tflops": flops_total / (sms * 1e-3) / 1e12,
-                          "int8_tops": 2.0 * ch * m * n * k / (g_ms / max(c_, 1) * 1e-3) / 1e12,
+                          "int8_tops": 2.0 * ch * m * n * k / (g_ms * 1e-3) / 1e12,
                           "ms_per_step": sms})
         line["sweep"] = sweep
 
@@ -455,15 +623,14 @@ def main():
     # (PAPER.md:548 reports 7.6x over it at s=3 on B200)
     if world == 1 and not args.no_sweep:
         try:
-            ad, bd = a_d[:m, :k], b_d[:k, :n]
-            torch.matmul(ad, bd)
+            torch.matmul(a_d, b_d)
             torch.cuda.synchronize()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             reps = 3
             e0.record()
             for _ in range(reps):
-                torch.matmul(ad, bd)
+                torch.matmul(a_d, b_d)
             e1.record()
             torch.cuda.synchronize()
             dms = e0.elapsed_time(e1) / reps
@@ -477,54 +644,131 @@ def main():
         except Exception as e:  # context only: never fail the bench line
             line["fp64_dgemm_reference"] = {"error": repr(e)}
 
-    # e2e through the host-pointer C-ABI call (pinned host buffers)
+    # e2e through the host-pointer C-ABI call: pinned buffers (the contract),
+    # and plain pageable arrays (what std::vector / numpy callers pass)
     if not args.no_e2e:
+        def e2e_run(a_src, b_src, c_dst, nsteps):
+            oz.multiply(a_src, b_src, mcfg, plan, out=c_dst)
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            for _ in range(nsteps):
+                oz.multiply(a_src, b_src, mcfg, plan, out=c_dst)
+            el = (time.perf_counter() - t0) / nsteps
+            if world > 1:
+                tt = torch.tensor([el], device=dev, dtype=torch.float64)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                el = float(tt.item())
+            return el
+        e2e_steps = max(3, args.steps // 4)
         a_p = torch.from_numpy(a_h).pin_memory().numpy()
         b_p = torch.from_numpy(b_h).pin_memory().numpy()
         c_p = torch.empty((m, n), dtype=torch.float64).pin_memory().numpy()
-        oz.multiply(a_p, b_p, mcfg, plan, out=c_p)
-        e2e_steps = max(3, args.steps // 4)
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            oz.multiply(a_p, b_p, mcfg, plan, out=c_p)
-        el = (time.perf_counter() - t0) / e2e_steps
-        if world > 1:
-            t = torch.tensor([el], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el = float(t.item())
+        el = e2e_run(a_p, b_p, c_p, e2e_steps)
         line["e2e"] = {"value": flops_total / el / 1e12, "unit": "TFLOP/s",
                        "h2d_bytes_per_step": 8 * (m * k + k * n), "d2h_bytes_per_step": 8 * m * n,
-                       "ms_per_step": el * 1e3, "api": "ozgpu_dgemm (host pointers, pinned)"}
+                       "ms_per_step": el * 1e3,
+                       "api": "ozgpu_dgemm (host pointers, pinned buffers), wall clock, max "
+                              "over ranks"}
+        del a_p, b_p, c_p
+        c_pg = np.empty((m, n))
+        el = e2e_run(a_h, b_h, c_pg, e2e_steps)
+        line["e2e_pageable"] = {"value": flops_total / el / 1e12, "unit": "TFLOP/s",
+                                "ms_per_step": el * 1e3,
+                                "api": "ozgpu_dgemm (host pointers, pageable numpy arrays)"}
+        del c_pg
 
     # CPU baseline: the reference itself on sampled blocks, rank 0 at N=1 only
+    def cpu_sample(a_, b_, sl, k_, m_, n_, c_dev):
+        from oracle import pyoracle
+        if not pyoracle.have_ref():
+            return None
+        threads = os.cpu_count() or 1
+        bs = sample_block(k_)
+        blocks = cpu_blocks(m_, n_, threads, bs)
+        c_ref, secs = pyoracle.ref_multiply_blocks(a_, b_, sl[0], sl[1], blocks, threads)
+        c_gpu = c_dev.cpu().numpy()
+        same = all(np.array_equal(c_ref[r0:r1, c0:c1].view(np.uint64),
+                                  c_gpu[r0:r1, c0:c1].view(np.uint64))
+                   for r0, r1, c0, c1 in blocks)
+        flops = sum(2.0 * (r1 - r0) * (c1 - c0) * k_ for r0, r1, c0, c1 in blocks)
+        return {"value": flops / secs / 1e12, "unit": "TFLOP/s", "cores": threads,
+                "kind": "reference", "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+                "sample": f"{len(blocks)} C blocks of {bs}x{bs} with full k={k_}, reference "
+                          f"multiply() (oracle/_ref) one std::thread per block on {threads} "
+                          f"threads of {cpu_model()}; {secs:.1f} s; rate extrapolates to the "
+                          f"full product (blocking is exact)",
+                "blocks_bit_exact_vs_gpu": bool(same), "blocks": len(blocks)}
+
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         try:
-            from oracle import pyoracle
-            if pyoracle.have_ref():
-                threads = os.cpu_count() or 1
-                bs = 64
-                blocks = cpu_blocks(m, n, threads, bs)
-                c_ref, secs = run_cpu_reference(a_h, b_h, slices, blocks, threads)
-                step(plan)  # C of the headline plan (the sweep overwrote c_d)
-                torch.cuda.synchronize()
-                c_gpu = c_d.cpu().numpy()
-                same = all(np.array_equal(c_ref[r0:r1, c0:c1].view(np.uint64),
-                                          c_gpu[r0:r1, c0:c1].view(np.uint64))
-                           for r0, r1, c0, c1 in blocks)
-                flops = sum(2.0 * (r1 - r0) * (c1 - c0) * k for r0, r1, c0, c1 in blocks)
-                line["cpu_baseline"] = {
-                    "value": flops / secs / 1e12, "unit": "TFLOP/s", "cores": threads,
-                    "kind": "reference",
-                    "sample": f"{len(blocks)} C blocks of {bs}x{bs} with full k={k}, reference "
-                              f"multiply() (oracle/_ref) one std::thread per block; "
-                              f"{secs:.1f} s; rate extrapolates to the full product",
-                    "blocks_bit_exact_vs_gpu": bool(same)}
-            else:
-                line["cpu_baseline"] = None
+            step(plan)  # C of the headline plan (the sweep overwrote c_d)
+            torch.cuda.synchronize()
+            line["cpu_baseline"] = cpu_sample(a_h, b_h, slices, k, m, n, c_d)
         except Exception as e:  # never let the baseline break the GPU line
             line["cpu_baseline"] = {"error": repr(e)}
+
+    # DRAM traffic of the pair GEMM, measured now by an ncu child run
+    if world == 1 and not args.no_traffic:
+        tr = measure_traffic(args.config)
+        if tr and tr.get("bytes"):
+            line["roofline"]["traffic"] = tr["bytes"]
+            line["roofline"]["traffic_detail"] = tr
+
+    # north-star sub-record: 16384^3 at the estimator's slices, own roofline
+    if world == 1 and args.config == "c2" and not args.no_north_star:
+        try:
+            ns = dict(CONFIGS["ns"])
+            a2, b2, m2, n2 = load_panels(ns)
+            a2h, b2h = a2.cpu().numpy(), b2.cpu().numpy()
+            sl2, est2 = estimate(ns, a2h, b2h)
+            p2 = oz.make_plan(mcfg, ns["k"], *sl2)
+            c2 = torch.empty((m2, n2), dtype=torch.float64, device=dev)
+            step2 = make_step(a2, b2, c2, m2, n2, ns["k"], exchange=False)
+            for _ in range(3):
+                step2(p2)
+            nsteps = 3
+            sampler.start()
+            ms2, _ = timed(nsteps, p2, step2)
+            clk2 = sampler.stop()
+            s2, g2, cc2 = stage_split(nsteps, p2, step2)
+            tops2, roofs2 = rooflines(m2, n2, ns["k"], sl2, g2, s2, cc2)
+            rec = {"workload": ns["name"], "slices": list(sl2), "chi": chi_of(*sl2),
+                   "estimator": est2, "steps": nsteps, "ms_per_step": ms2,
+                   "value": 2.0 * m2 * n2 * ns["k"] / (ms2 * 1e-3) / 1e12, "unit": "TFLOP/s",
+                   "int8_tops": tops2, "frac_of_4500_tops_spec": tops2 / 4500.0,
+                   "stage_ms": {"slicing": s2, "pair_gemms": g2, "combine": cc2},
+                   **roofs2, "clocks": clk2}
+            if not args.no_cpu_baseline:
+                step2(p2)
+                torch.cuda.synchronize()
+                rec["cpu_baseline"] = cpu_sample(a2h, b2h, sl2, ns["k"], m2, n2, c2)
+            line["north_star"] = rec
+        except Exception as e:
+            line["north_star"] = {"error": repr(e)}
+
+    # weak-scaling sub-record at N > 1: every rank an 8192^3 block (configs[1])
+    if world > 1 and args.config == "c5":
+        try:
+            wc = dict(CONFIGS["c2"])
+            aw, bw, mw, nw = load_panels(wc)
+            slw, _ = estimate(wc, aw.cpu().numpy(), bw.cpu().numpy())
+            pw = oz.make_plan(mcfg, wc["k"], *slw)
+            cw = torch.empty((mw, nw), dtype=torch.float64, device=dev)
+            stepw = make_step(aw, bw, cw, mw, nw, wc["k"])
+            for _ in range(3):
+                stepw(pw)
+            nsteps = max(3, args.steps // 4)
+            msw, _ = timed(nsteps, pw, stepw)
+            pr, pc = shard.grid_for(world)
+            tot = 2.0 * pr * wc["m"] * pc * wc["n"] * wc["k"]
+            line["weak_scaling"] = {"workload": "configs[1] block (8192^3) per rank, panels "
+                                                "broadcast from their owners each step",
+                                    "slices": list(slw), "ms_per_step": msw,
+                                    "value": tot / (msw * 1e-3) / 1e12, "unit": "TFLOP/s",
+                                    "global_m": pr * wc["m"], "global_n": pc * wc["n"]}
+        except Exception as e:
+            line["weak_scaling"] = {"error": repr(e)}
 
     if rank == 0:
         print(json.dumps(line))

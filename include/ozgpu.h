@@ -21,7 +21,16 @@
  *   orientation: 0 rows (left factor), 1 columns (right factor)
  *
  * Threading: every call is safe from any number of host threads
- * (SPEC.md:91,363-364); calls on one context serialise on its stream.
+ * (SPEC.md:91,363-364).  A context owns one workspace (slices, scales, chunk
+ * planes, lockstep counters); every call orders its use of it after the
+ * previous call's on the GPU (an event recorded where that call's work was
+ * enqueued, waited on by this call's stream), so device-pointer calls on
+ * different streams never overwrite each other's workspace -- on one context
+ * they run one after the other.  Use one context per stream to overlap them.
+ *
+ * Operands: leading dimensions must be >= the row length (lda >= k,
+ * ldb >= n, ldc >= n) and pointers non-null when the operand has elements,
+ * else OZGPU_INVALID_ARGUMENT before anything is copied or launched.
  */
 #ifndef OZGPU_H
 #define OZGPU_H
@@ -167,7 +176,11 @@ int ozgpu_fp64_gemm(ozgpu_ctx* ctx, int absolute, int64_t m, int64_t k, int64_t 
 /* ---- the GEMM (multiply, proj/src/scheme.cpp:219-361) ------------------ */
 /* Host buffers: A m x k (lda), B k x n (ldb), C m x n (ldc), all row-major
  * binary64.  Copies in, runs slicing + int8 tcgen05 pair GEMMs + exact
- * epilogue on the GPU, copies C out.  diag may be NULL. */
+ * epilogue on the GPU, copies C out.  diag may be NULL.  On an input error
+ * (Inf / NaN / -0, scheme.cpp:223-225) C is left untouched, except that
+ * page-locked buffers of a product >= 64 MiB stream C back block by block
+ * while later blocks are still being checked: there its contents are then
+ * unspecified. */
 int ozgpu_dgemm(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda,
                 const double* b, int64_t ldb, double* c, int64_t ldc, ozgpu_mma_config cfg,
                 const ozgpu_plan* plan, ozgpu_diag* diag);
@@ -194,6 +207,28 @@ int ozgpu_dgemm_device(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const do
 int ozgpu_split(ozgpu_ctx* ctx, int orientation, int64_t rows, int64_t cols, const double* x,
                 int64_t ldx, int width, int count, int mode, int64_t* slices_out,
                 int* scales_out);
+/* The production int8 slicer (the kernels ozgpu_dgemm* launch for its
+ * operands: rowmax + streaming row slicer for A, column max + transposing
+ * column slicer for B in truncate mode at t <= 7; generic kernels otherwise)
+ * with its output as the GEMM reads it: slices_out [count][blocks][ld] int8,
+ * K-major (blocks = rows for orientation 0, cols for 1; ld a multiple of 128
+ * >= the block length, the tail zero-filled), scales_out per block.
+ * Bit-exact against split_rows / split_cols (slicing.cpp:67-132). */
+int ozgpu_split_i8(ozgpu_ctx* ctx, int orientation, int64_t rows, int64_t cols, const double* x,
+                   int64_t ldx, int width, int count, int mode, int8_t* slices_out, int64_t ld,
+                   int* scales_out);
+/* The production pair GEMM's output before the combine: runs the slicing and
+ * the tcgen05 pair-GEMM launch ozgpu_dgemm would make (same kernel choice,
+ * chunk bins, lockstep and split-k tail; never row-blocked) and copies the
+ * int32 chunk planes out.  Chunk c holds sum_{p < npairs} E_{l0+p, d+2-l0-p}
+ * (integer_gemm of the slice pair, mma_sim.cpp:76-125, scheme.cpp:252-262).
+ * *nchunks_out = chunk count; chunk_table (may be NULL) gets up to max_chunks
+ * triples (d, l0, npairs); planes_out (NULL = query only) receives the window
+ * rows [r0, r1) x columns [c0, c1) of every plane, [nchunks][r1-r0][c1-c0]. */
+int ozgpu_pair_planes(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a,
+                      int64_t lda, const double* b, int64_t ldb, ozgpu_mma_config cfg,
+                      const ozgpu_plan* plan, int* nchunks_out, int* chunk_table, int max_chunks,
+                      int64_t r0, int64_t r1, int64_t c0, int64_t c1, int32_t* planes_out);
 /* integer_gemm, proj/src/mma_sim.cpp:76-125: exact X (m x k) * Y (k x n)
  * on the tcgen05 int8 path (int32 accumulation in TMEM); when the inputs
  * do not fit int8 or the bound k*max|x|*max|y| can exceed I_T, an exact

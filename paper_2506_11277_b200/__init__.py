@@ -36,7 +36,7 @@ __all__ = [
     "multiply_axpby", "multiply_device", "select_slices", "scaling_profile", "split_rows",
     "split_cols", "integer_gemm", "chi", "plan_levels", "spare_carries",
     "diagonal_flush_threshold", "optimal_slice_width", "max_inner_dim", "random_uniform",
-    "gen_kappa_d", "kernel_launches", "library_path",
+    "gen_kappa_d", "kernel_launches", "library_path", "split_i8", "pair_planes",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -562,6 +562,56 @@ def integer_gemm(x, y, cfg: MmaConfig, c=None, device: Optional[int] = None) -> 
                                    cp.ctypes.data_as(P) if cp is not None else None,
                                    out.ctypes.data_as(P), cfg._c()))
     return out
+
+
+_sig("ozgpu_split_i8", ctypes.c_int, _P, ctypes.c_int, _I64, _I64, _DP, _I64, ctypes.c_int,
+     ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int8), _I64, ctypes.POINTER(ctypes.c_int))
+_sig("ozgpu_pair_planes", ctypes.c_int, _P, _I64, _I64, _I64, _DP, _I64, _DP, _I64, _Cfg,
+     ctypes.POINTER(_Plan), ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+     ctypes.c_int, _I64, _I64, _I64, _I64, ctypes.POINTER(ctypes.c_int32))
+
+
+def split_i8(x, width: int, count: int, orientation: BlockOrientation,
+             mode: SliceMode = SliceMode.TRUNCATE, device: Optional[int] = None):
+    """The production int8 slicer (what multiply() runs on its operands) ->
+    (slices [count, blocks, ld] int8, K-major with a zero-filled tail, scales).
+    Bit-exact against split_rows / split_cols (slicing.cpp:67-132)."""
+    x = _f64(x)
+    rows, cols = x.shape
+    blocks, length = (rows, cols) if int(orientation) == 0 else (cols, rows)
+    ld = max(128, -(-length // 128) * 128)
+    out = np.empty((count, blocks, ld), dtype=np.int8)
+    scales = np.zeros(blocks, dtype=np.int32)
+    _check(_lib.ozgpu_split_i8(_ctx(device), int(orientation), rows, cols, _dp(x), cols, width,
+                               count, int(mode), out.ctypes.data_as(ctypes.POINTER(ctypes.c_int8)),
+                               ld, scales.ctypes.data_as(ctypes.POINTER(ctypes.c_int))))
+    return out, scales
+
+
+def pair_planes(a, b, cfg: MmaConfig, plan: MultiplyPlan, window=None,
+                device: Optional[int] = None):
+    """The production pair GEMM's int32 chunk planes (before the combine) ->
+    (planes [nchunks, rows, cols] int32 over `window` = (r0, r1, c0, c1),
+    default all of C; chunks [(d, l0, npairs)]): chunk c is the exact sum of
+    integer_gemm(A_l, B_h) over its pairs (l0 + p, d + 2 - l0 - p)."""
+    a, b = _f64(a), _f64(b)
+    if a.shape[1] != b.shape[0]:
+        raise InvalidArgument("pair_planes: shape mismatch")
+    m, k = a.shape
+    n = b.shape[1]
+    r0, r1, c0, c1 = window if window is not None else (0, m, 0, n)
+    pc = plan._c()
+    nc = ctypes.c_int()
+    _check(_lib.ozgpu_pair_planes(_ctx(device), m, n, k, _dp(a), k, _dp(b), n, cfg._c(),
+                                  ctypes.byref(pc), ctypes.byref(nc), None, 0, 0, 0, 0, 0, None))
+    table = (ctypes.c_int * (3 * max(nc.value, 1)))()
+    planes = np.zeros((nc.value, r1 - r0, c1 - c0), dtype=np.int32)
+    _check(_lib.ozgpu_pair_planes(_ctx(device), m, n, k, _dp(a), k, _dp(b), n, cfg._c(),
+                                  ctypes.byref(pc), ctypes.byref(nc), table, nc.value,
+                                  r0, r1, c0, c1,
+                                  planes.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))))
+    chunks = [(table[3 * c], table[3 * c + 1], table[3 * c + 2]) for c in range(nc.value)]
+    return planes, chunks
 
 
 # -------------------------------------------------------------- generators

@@ -111,12 +111,19 @@ struct DevBuf {
 struct PinnedBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  // nullptr when the page-locked allocation fails (the caller then copies
+  // from the pageable buffers directly); the runtime's sticky last error is
+  // cleared so the failure cannot leak into a later, valid call.
   void* get(size_t want) {
     if (want > bytes) {
       if (p) cudaFreeHost(p);
       p = nullptr;
       bytes = 0;
-      OZ_CUDA(cudaMallocHost(&p, want));
+      if (cudaMallocHost(&p, want) != cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+        return nullptr;
+      }
       bytes = want;
     }
     return p;
@@ -168,6 +175,19 @@ struct ozgpu_ctx {
   std::vector<cudaEvent_t> pipe_events;
   // pinned staging of pageable host A / B / C (ozgpu_dgemm)
   ozgpu::PinnedBuf stage_a, stage_b, stage_c;
+  // Workspace ordering across streams: every call that touches the
+  // workspace first makes its stream wait on ws_done (recorded where the
+  // previous call's last use of the workspace was enqueued), and records it
+  // again after its own enqueue.  ozgpu_dgemm_device returns without
+  // synchronising, so without this a call on another stream (or the host
+  // path on ctx->stream) could overwrite slices / planes still in use.
+  cudaEvent_t ws_done = nullptr;
+  bool ws_recorded = false;
+  // debug hook ozgpu_pair_planes: run_multiply stops after the pair GEMM
+  // (split mode, no row blocking) and leaves the int32 chunk planes in
+  // `planes` with this geometry
+  bool debug_planes = false;
+  int64_t dbg_plane_stride = 0, dbg_ldp = 0;
   // stage timing (ozgpu_set_stage_timing)
   bool timing = false;
   std::vector<std::array<cudaEvent_t, 4>> pending_events;
@@ -204,6 +224,21 @@ void init_ctx(ozgpu_ctx* ctx, int device) {
   if (!fn || q != cudaDriverEntryPointSuccess)
     throw DeviceError("cuTensorMapEncodeTiled unavailable from the driver");
   ctx->encode = reinterpret_cast<EncodeTiledFn>(fn);
+}
+
+// Orders this call's use of the context workspace after every earlier
+// call's (caller holds ctx->mu; `st` is the stream the call enqueues its
+// first workspace access on -- helper streams fork from it by events).
+void acquire_workspace(ozgpu_ctx* ctx, cudaStream_t st) {
+  if (ctx->ws_recorded) OZ_CUDA(cudaStreamWaitEvent(st, ctx->ws_done, 0));
+}
+
+// Marks the end of this call's workspace use on `st` (every helper stream
+// has been joined back into `st` by then).
+void release_workspace(ozgpu_ctx* ctx, cudaStream_t st) {
+  if (!ctx->ws_done) OZ_CUDA(cudaEventCreateWithFlags(&ctx->ws_done, cudaEventDisableTiming));
+  OZ_CUDA(cudaEventRecord(ctx->ws_done, st));
+  ctx->ws_recorded = true;
 }
 
 // TMA L2 sector promotion of the slice loads (OZGPU_L2_PROMO=0/64/128/256).
@@ -614,7 +649,7 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
   // bytes (72 GiB for 32768^3 at (13,12)); beyond the budget the GEMM +
   // combine run over row blocks of C against the slices already in HBM
   // (blocking is exact: scales are per row of A / column of B).
-  if (p.strategy == 2 && m > 512 && n > 0 && !cp.chunks.empty()) {
+  if (p.strategy == 2 && m > 512 && n > 0 && !cp.chunks.empty() && !ctx->debug_planes) {
     const int64_t ldp_b = round_up(n, 4);
     const double plane_bytes = 4.0 * static_cast<double>(cp.chunks.size()) * m * ldp_b;
     double budget = 0.0;
@@ -659,7 +694,7 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
     // L2 (105 GB vs 66 GB DRAM per launch) and loses to split + combine.
     int words = p.strategy == 2 ? exact_words(cp.diagonals, t, cp.chunks.size()) : 0;
     bool fused = false;
-    if (const char* env = std::getenv("OZGPU_EPILOGUE")) {
+    if (const char* env = ctx->debug_planes ? nullptr : std::getenv("OZGPU_EPILOGUE")) {
       if (std::string(env) == "split") fused = false;
       if (std::string(env) == "fused" && p.strategy == 2 && words <= 3) fused = true;
     }
@@ -817,7 +852,7 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
       // than split + the combine kernel under the B200 power cap (the heavy
       // epilogue competes with the MMAs for power), so not the default.
       bool final_mode = false;
-      if (const char* env = std::getenv("OZGPU_EPILOGUE"))
+      if (const char* env = ctx->debug_planes ? nullptr : std::getenv("OZGPU_EPILOGUE"))
         final_mode = std::string(env) == "final" && p.strategy == 2 && g.nchunks >= 2 &&
                      cp.diagonals <= 64 &&
                      static_cast<int64_t>(cp.diagonals - 1) * t + 40 <= 126;
@@ -898,6 +933,16 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
       }
     }
     if (ctx->timing) OZ_CUDA(cudaEventRecord(ev[2], st));
+    if (ctx->debug_planes) {
+      ctx->dbg_plane_stride = plane;
+      ctx->dbg_ldp = ldp;
+      if (ctx->timing) {
+        OZ_CUDA(cudaEventRecord(ev[3], st));
+        ctx->pending_events.push_back(ev);
+      }
+      ctx->launches += launches;
+      return nullptr;
+    }
 
     CombineArgs c{};
     c.planes = planes;
@@ -959,6 +1004,26 @@ void check_plan(const ozgpu_plan* plan) {
   if (!plan) throw std::invalid_argument("multiply: null plan");
   if (plan->strategy < 0 || plan->strategy > 2)
     throw std::invalid_argument("multiply: unknown accumulation strategy");
+}
+
+// C-ABI operand checks (no reference counterpart: its Matrix carries its own
+// shape): leading dimensions cover the rows, pointers are non-null whenever
+// the operand has elements.  Raised before any copy or launch.
+void check_operands(const char* fn, int64_t m, int64_t n, int64_t k, const void* a, int64_t lda,
+                    const void* b, int64_t ldb, const void* c, int64_t ldc) {
+  const std::string f(fn);
+  if (m < 0 || n < 0 || k < 0) throw std::invalid_argument(f + ": shape mismatch");
+  if (lda < k)
+    throw std::invalid_argument(f + ": leading dimension of A (" + std::to_string(lda) +
+                                ") is smaller than k (" + std::to_string(k) + ")");
+  if (ldb < n)
+    throw std::invalid_argument(f + ": leading dimension of B (" + std::to_string(ldb) +
+                                ") is smaller than n (" + std::to_string(n) + ")");
+  if (ldc < n)
+    throw std::invalid_argument(f + ": leading dimension of C (" + std::to_string(ldc) +
+                                ") is smaller than n (" + std::to_string(n) + ")");
+  if ((m > 0 && k > 0 && !a) || (k > 0 && n > 0 && !b) || (m > 0 && n > 0 && !c))
+    throw std::invalid_argument(f + ": null matrix pointer");
 }
 
 // Errors the reference raises from split() after multiply's own validation
@@ -1036,6 +1101,11 @@ void host_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double
   double* sa = static_cast<double*>(ctx->stage_a.get(sizeof(double) * m * k));
   double* sb = static_cast<double*>(ctx->stage_b.get(sizeof(double) * k * n));
   double* sc = static_cast<double*>(ctx->stage_c.get(sizeof(double) * m * n));
+  if (!sa || !sb || !sc) {  // no page-locked memory: the driver's own staging
+    host_multiply_locked(ctx, m, n, k, a, lda, b, ldb, c, ldc, cfg, p, diag, axpby, alpha, beta,
+                         cin, ldcin);
+    return;
+  }
   std::thread tb([&] { parallel_copy(sb, n, b, ldb, k, n); });
   parallel_copy(sa, k, a, lda, m, k);
   tb.join();
@@ -1050,6 +1120,7 @@ void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const
                           bool axpby, double alpha, double beta, const double* cin,
                           int64_t ldcin) {
   cudaStream_t st = ctx->stream;
+  acquire_workspace(ctx, st);
   ValidationResult v = host_validation(cfg, p, k);
   double* da = static_cast<double*>(ctx->in_a.get(sizeof(double) * m * k + 8));
   double* db = static_cast<double*>(ctx->in_b.get(sizeof(double) * k * n + 8));
@@ -1301,12 +1372,15 @@ void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const
   }
   int* psi_dev = run_multiply(ctx, m, n, k, da, k, db, n, dc, n, cfg, p, st, nullptr, axpby,
                               alpha, beta, dcin, n);
-  d2h(c, ldc, dc, m, n, st);
   int hs = 0, hpsi = 0;
   OZ_CUDA(cudaMemcpyAsync(&hs, ctx->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   if (psi_dev) OZ_CUDA(cudaMemcpyAsync(&hpsi, psi_dev, sizeof(int), cudaMemcpyDeviceToHost, st));
   OZ_CUDA(cudaStreamSynchronize(st));
+  // the reference throws before producing output (scheme.cpp:223-225): C is
+  // copied back only for clean inputs
   if (hs) throw std::invalid_argument("multiply: inputs must be finite with no negative zeros");
+  d2h(c, ldc, dc, m, n, st);
+  OZ_CUDA(cudaStreamSynchronize(st));
   if (diag) *diag = make_diag(p, cfg, m, n, k, hpsi);
 }
 
@@ -1514,6 +1588,7 @@ int ozgpu_scaling_profile(ozgpu_ctx* ctx, int64_t m, int64_t k, int64_t n, const
     std::lock_guard<std::mutex> lock(ctx->mu);
     OZ_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t st = ctx->stream;
+    acquire_workspace(ctx, st);
     int64_t launches = 0;
     double* da = static_cast<double*>(ctx->in_a.get(sizeof(double) * m * k + 8));
     double* db = static_cast<double*>(ctx->in_b.get(sizeof(double) * k * n + 8));
@@ -1565,6 +1640,7 @@ int ozgpu_block_ratios(ozgpu_ctx* ctx, int orientation, int64_t rows, int64_t co
     std::lock_guard<std::mutex> lock(ctx->mu);
     OZ_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t st = ctx->stream;
+    acquire_workspace(ctx, st);
     int64_t launches = 0;
     double* dx = static_cast<double*>(ctx->in_a.get(sizeof(double) * rows * cols + 8));
     h2d(dx, x, rows, cols, ldx, st);
@@ -1614,6 +1690,7 @@ int ozgpu_fp64_gemm(ozgpu_ctx* ctx, int absolute, int64_t m, int64_t k, int64_t 
     std::lock_guard<std::mutex> lock(ctx->mu);
     OZ_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t st = ctx->stream;
+    acquire_workspace(ctx, st);
     int64_t launches = 0;
     double* da = static_cast<double*>(ctx->in_a.get(sizeof(double) * m * k + 8));
     double* db = static_cast<double*>(ctx->in_b.get(sizeof(double) * k * n + 8));
@@ -1633,7 +1710,7 @@ int ozgpu_dgemm(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a
   return guarded([&] {
     if (!ctx) throw std::invalid_argument("multiply: null context");
     check_plan(plan);
-    if (m < 0 || n < 0 || k < 0) throw std::invalid_argument("multiply: shape mismatch");
+    check_operands("multiply", m, n, k, a, lda, b, ldb, c, ldc);
     host_multiply(ctx, m, n, k, a, lda, b, ldb, c, ldc, cfg, *plan, diag, false, 1.0, 0.0,
                   nullptr, 0);
   });
@@ -1646,7 +1723,9 @@ int ozgpu_dgemm_axpby(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, double al
   return guarded([&] {
     if (!ctx) throw std::invalid_argument("multiply_axpby: null context");
     check_plan(plan);
-    if (m < 0 || n < 0 || k < 0) throw std::invalid_argument("multiply_axpby: shape mismatch");
+    check_operands("multiply_axpby", m, n, k, a, lda, b, ldb, d_out, ldd);
+    if (ldc < n) throw std::invalid_argument("multiply_axpby: leading dimension of C_in is smaller than n");
+    if (m > 0 && n > 0 && !c_in) throw std::invalid_argument("multiply_axpby: null matrix pointer");
     host_multiply(ctx, m, n, k, a, lda, b, ldb, d_out, ldd, cfg, *plan, diag, true, alpha, beta,
                   c_in, ldc);
   });
@@ -1659,7 +1738,7 @@ int ozgpu_dgemm_device(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const do
   return guarded([&] {
     if (!ctx) throw std::invalid_argument("multiply: null context");
     check_plan(plan);
-    if (m < 0 || n < 0 || k < 0) throw std::invalid_argument("multiply: shape mismatch");
+    check_operands("multiply", m, n, k, a, lda, b, ldb, c, ldc);
     if (k < 1) throw std::invalid_argument("multiply: empty inner dimension");
     ValidationResult v = host_validation(cfg, *plan, k);
     if (v.capacity_error || v.precision_error) throw std::domain_error(v.message);
@@ -1668,6 +1747,7 @@ int ozgpu_dgemm_device(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const do
     std::lock_guard<std::mutex> lock(ctx->mu);
     OZ_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t st = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
+    acquire_workspace(ctx, st);
     // Repeated calls with the same shape, plan, pointers and stream replay a
     // captured CUDA graph (one launch instead of ~10 enqueues and the host
     // planning); the first call runs eagerly (it also sizes the workspace),
@@ -1700,6 +1780,7 @@ int ozgpu_dgemm_device(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const do
       const uint64_t gen = g_workspace_gen.load();
       if (e.exec && e.gen == gen) {
         OZ_CUDA(cudaGraphLaunch(e.exec, st));
+        release_workspace(ctx, st);
         ctx->launches += e.launches;
         if (diag) *diag = make_diag(*plan, cfg, m, n, k, 0);
         return;
@@ -1738,14 +1819,21 @@ int ozgpu_dgemm_device(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const do
           e.uses = 1;
         } else {
           OZ_CUDA(cudaGraphLaunch(e.exec, st));
+          release_workspace(ctx, st);
           ctx->launches += e.launches;
           if (diag) *diag = make_diag(*plan, cfg, m, n, k, 0);
           return;
         }
       }
     }
-    run_multiply(ctx, m, n, k, a, lda, b, ldb, c, ldc, cfg, *plan, st, dev_status, false, 1.0,
-                 0.0, nullptr, 0);
+    try {
+      run_multiply(ctx, m, n, k, a, lda, b, ldb, c, ldc, cfg, *plan, st, dev_status, false, 1.0,
+                   0.0, nullptr, 0);
+    } catch (...) {
+      release_workspace(ctx, st);  // whatever was enqueued still orders later calls
+      throw;
+    }
+    release_workspace(ctx, st);
     if (diag) *diag = make_diag(*plan, cfg, m, n, k, 0);
   });
 }
@@ -1761,6 +1849,7 @@ int ozgpu_split(ozgpu_ctx* ctx, int orientation, int64_t rows, int64_t cols, con
     std::lock_guard<std::mutex> lock(ctx->mu);
     OZ_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t st = ctx->stream;
+    acquire_workspace(ctx, st);
     int64_t launches = 0;
     double* dx = static_cast<double*>(ctx->in_a.get(sizeof(double) * rows * cols + 8));
     h2d(dx, x, rows, cols, ldx, st);
@@ -1801,6 +1890,113 @@ int ozgpu_split(ozgpu_ctx* ctx, int orientation, int64_t rows, int64_t cols, con
   });
 }
 
+int ozgpu_split_i8(ozgpu_ctx* ctx, int orientation, int64_t rows, int64_t cols, const double* x,
+                   int64_t ldx, int width, int count, int mode, int8_t* slices_out, int64_t ld,
+                   int* scales_out) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("split: null context");
+    if (width < 1 || width > 62) throw std::invalid_argument("split: width out of range");
+    if (count < 1) throw std::invalid_argument("split: need at least one slice");
+    if (mode == 1 && width < 2) throw std::invalid_argument("split: nearest mode needs width >= 2");
+    if (width > 7)
+      throw std::invalid_argument("split_i8: width " + std::to_string(width) +
+                                  " does not fit the int8 operand");
+    if (rows < 0 || cols < 0 || ldx < cols) throw std::invalid_argument("split_i8: bad shape");
+    const int64_t blocks = orientation == 0 ? rows : cols;
+    const int64_t len = orientation == 0 ? cols : rows;
+    if (ld < round_up(std::max<int64_t>(len, 1), kKPad) || ld % kKPad)
+      throw std::invalid_argument("split_i8: ld must be a multiple of 128 covering the block length");
+    if ((rows * cols > 0 && !x) || (blocks > 0 && (!slices_out || !scales_out)))
+      throw std::invalid_argument("split_i8: null pointer");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    OZ_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    acquire_workspace(ctx, st);
+    int64_t launches = 0;
+    double* dx = static_cast<double*>(ctx->in_a.get(sizeof(double) * rows * cols + 8));
+    h2d(dx, x, rows, cols, ldx, st);
+    int* status = static_cast<int*>(ctx->status.get(sizeof(int)));
+    OZ_CUDA(cudaMemsetAsync(status, 0, sizeof(int), st));
+    const size_t bytes = static_cast<size_t>(count) * blocks * ld;
+    int8_t* out = static_cast<int8_t*>(ctx->slices_a.get(bytes + 1));
+    int* scales = static_cast<int*>(ctx->qa.get(sizeof(int) * (blocks + 1)));
+    // exactly the launches run_multiply makes for its operands
+    if (orientation == 0) {
+      OZ_CUDA(launch_slice_rows(dx, cols, rows, cols, ld, width, count, mode, out, 0, scales,
+                                status, st, &launches));
+    } else {
+      auto* colmax = static_cast<unsigned long long*>(ctx->colmax.get(8 * (cols + 1)));
+      OZ_CUDA(launch_slice_cols(dx, cols, rows, cols, ld, width, count, mode, out, 0, scales,
+                                colmax, status, st, &launches));
+    }
+    int hs = 0;
+    if (bytes) OZ_CUDA(cudaMemcpyAsync(slices_out, out, bytes, cudaMemcpyDeviceToHost, st));
+    if (blocks)
+      OZ_CUDA(cudaMemcpyAsync(scales_out, scales, sizeof(int) * blocks, cudaMemcpyDeviceToHost, st));
+    OZ_CUDA(cudaMemcpyAsync(&hs, status, sizeof(int), cudaMemcpyDeviceToHost, st));
+    OZ_CUDA(cudaStreamSynchronize(st));
+    ctx->launches += launches;
+    if (hs & 1) throw std::invalid_argument("split: non-finite entry");
+  });
+}
+
+int ozgpu_pair_planes(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a,
+                      int64_t lda, const double* b, int64_t ldb, ozgpu_mma_config cfg,
+                      const ozgpu_plan* plan, int* nchunks_out, int* chunk_table, int max_chunks,
+                      int64_t r0, int64_t r1, int64_t c0, int64_t c1, int32_t* planes_out) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("pair_planes: null context");
+    check_plan(plan);
+    if (!nchunks_out) throw std::invalid_argument("pair_planes: null argument");
+    check_operands("pair_planes", m, n, k, a, lda, b, ldb, planes_out ? static_cast<const void*>(planes_out) : static_cast<const void*>(a), n);
+    if (k < 1) throw std::invalid_argument("multiply: empty inner dimension");
+    ValidationResult v = host_validation(cfg, *plan, k);
+    if (v.capacity_error || v.precision_error) throw std::domain_error(v.message);
+    const std::string perr = plan_error(*plan);
+    if (!perr.empty()) throw std::invalid_argument(perr);
+    const ChunkPlan cp = build_chunks(*plan, cfg, k);
+    const int nc = static_cast<int>(cp.chunks.size());
+    *nchunks_out = nc;
+    if (chunk_table)
+      for (int c = 0; c < std::min(nc, max_chunks); ++c) {
+        chunk_table[3 * c] = cp.chunks[c].d;
+        chunk_table[3 * c + 1] = cp.chunks[c].l0;
+        chunk_table[3 * c + 2] = cp.chunks[c].npairs;
+      }
+    if (!planes_out || m == 0 || n == 0 || nc == 0) return;
+    if (r0 < 0 || r1 > m || r0 >= r1 || c0 < 0 || c1 > n || c0 >= c1)
+      throw std::invalid_argument("pair_planes: window outside C");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    OZ_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    acquire_workspace(ctx, st);
+    double* da = static_cast<double*>(ctx->in_a.get(sizeof(double) * m * k + 8));
+    double* db = static_cast<double*>(ctx->in_b.get(sizeof(double) * k * n + 8));
+    double* dc = static_cast<double*>(ctx->io_c.get(sizeof(double) * m * n + 8));
+    h2d(da, a, m, k, lda, st);
+    h2d(db, b, k, n, ldb, st);
+    struct Guard {
+      ozgpu_ctx* c;
+      ~Guard() { c->debug_planes = false; }
+    } guard{ctx};
+    ctx->debug_planes = true;
+    run_multiply(ctx, m, n, k, da, k, db, n, dc, n, cfg, *plan, st, nullptr, false, 1.0, 0.0,
+                 nullptr, 0);
+    const int32_t* planes = static_cast<const int32_t*>(ctx->planes.p);
+    const int64_t wr = r1 - r0, wc = c1 - c0;
+    for (int c = 0; c < nc; ++c)
+      OZ_CUDA(cudaMemcpy2DAsync(planes_out + static_cast<int64_t>(c) * wr * wc,
+                                wc * sizeof(int32_t),
+                                planes + c * ctx->dbg_plane_stride + r0 * ctx->dbg_ldp + c0,
+                                ctx->dbg_ldp * sizeof(int32_t), wc * sizeof(int32_t), wr,
+                                cudaMemcpyDeviceToHost, st));
+    int hs = 0;
+    OZ_CUDA(cudaMemcpyAsync(&hs, ctx->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    OZ_CUDA(cudaStreamSynchronize(st));
+    if (hs) throw std::invalid_argument("multiply: inputs must be finite with no negative zeros");
+  });
+}
+
 int ozgpu_integer_gemm(ozgpu_ctx* ctx, int64_t m, int64_t k, int64_t n, const int64_t* x,
                        const int64_t* y, const int64_t* c, int64_t* out, ozgpu_mma_config cfg) {
   return guarded([&] {
@@ -1831,6 +2027,7 @@ int ozgpu_integer_gemm(ozgpu_ctx* ctx, int64_t m, int64_t k, int64_t n, const in
     std::lock_guard<std::mutex> lock(ctx->mu);
     OZ_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t st = ctx->stream;
+    acquire_workspace(ctx, st);
     int64_t launches = 0;
     if (m == 0 || n == 0) return;
     int64_t* dx = static_cast<int64_t*>(ctx->i64a.get(sizeof(int64_t) * m * k + 8));

@@ -1,0 +1,104 @@
+"""C-ABI contract on the GPU: the workspace ordering across streams (the
+reference's multiply is called from host thread pools, main.cpp:422,486,557,
+and must stay deterministic), operand validation, and
+C left untouched when the inputs are rejected (scheme.cpp:223-225)."""
+import ctypes
+
+import numpy as np
+import pytest
+
+from helpers import bits_equal, mismatch_report, random_matrix, uniform
+
+pytestmark = pytest.mark.gpu
+
+
+def test_device_calls_on_two_streams_and_host_call_are_ordered(oz, ref):
+    """ozgpu_dgemm_device returns without synchronising; two calls on
+    different streams with different inputs and plans, followed at once by a
+    host-pointer multiply, all share the context's workspace.  Each result must
+    equal its own serial result bitwise (eager, graph capture and replays)."""
+    import torch
+    rng = np.random.default_rng(123)
+    cfg = oz.MmaConfig.int8_int32()
+    dev = torch.device("cuda:0")
+    m, k, n = 1536, 2048, 1280
+    a1, b1 = uniform(m, k, rng), uniform(k, n, rng)
+    a2, b2 = random_matrix(m, k, rng, -9, 9, 0.01), random_matrix(k, n, rng, -9, 9, 0.01)
+    a3, b3 = uniform(700, 900, rng), uniform(900, 650, rng)
+    p1, p2, p3 = oz.make_plan(cfg, k, 12, 11), oz.make_plan(cfg, k, 9, 9), oz.make_plan(cfg, 900, 7, 6)
+    want1 = oz.multiply(a1, b1, cfg, p1).c
+    want2 = oz.multiply(a2, b2, cfg, p2).c
+    want3 = oz.multiply(a3, b3, cfg, p3).c
+    # anchor the serial results on the reference (corner blocks)
+    blocks = [(0, 16, 0, 16), (m - 16, m, n - 16, n)]
+    r1, _ = ref.ref_multiply_blocks(a1, b1, 12, 11, blocks, 2)
+    for r0, r1_, c0, c1 in blocks:
+        assert bits_equal(want1[r0:r1_, c0:c1], r1[r0:r1_, c0:c1])
+    s1, s2 = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    A1, B1 = torch.from_numpy(a1).to(dev), torch.from_numpy(b1).to(dev)
+    A2, B2 = torch.from_numpy(a2).to(dev), torch.from_numpy(b2).to(dev)
+    C1 = torch.empty(m, n, dtype=torch.float64, device=dev)
+    C2 = torch.empty(m, n, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    for it in range(4):  # eager, capture, replay, replay on each stream
+        C1.fill_(0.0)
+        C2.fill_(0.0)
+        torch.cuda.synchronize()
+        oz.multiply_device(m, n, k, A1.data_ptr(), k, B1.data_ptr(), n, C1.data_ptr(), n, cfg, p1,
+                           stream=s1.cuda_stream)
+        oz.multiply_device(m, n, k, A2.data_ptr(), k, B2.data_ptr(), n, C2.data_ptr(), n, cfg, p2,
+                           stream=s2.cuda_stream)
+        got3 = oz.multiply(a3, b3, cfg, p3).c  # host path on the context's own stream
+        torch.cuda.synchronize()
+        got1, got2 = C1.cpu().numpy(), C2.cpu().numpy()
+        assert bits_equal(got1, want1), (it, mismatch_report(got1, want1))
+        assert bits_equal(got2, want2), (it, mismatch_report(got2, want2))
+        assert bits_equal(got3, want3), (it, mismatch_report(got3, want3))
+
+
+def test_operand_validation(oz):
+    """lda < k, ldb < n, ldc < n and null pointers are rejected before any
+    copy or launch (C-ABI contract; the reference's Matrix carries its shape)."""
+    lib = oz._lib
+    cfg = oz.MmaConfig.int8_int32()
+    plan = oz.make_plan(cfg, 8, 2, 2)._c()
+    a = np.ones((4, 8))
+    b = np.ones((8, 6))
+    c = np.zeros((4, 6))
+    ctx = oz._ctx()
+    dp = oz._dp
+    cases = [(8, 6, 6, "", "ok"), (7, 6, 6, "leading dimension of A", "lda"),
+             (8, 5, 6, "leading dimension of B", "ldb"), (8, 6, 5, "leading dimension of C", "ldc")]
+    for lda, ldb, ldc, msg, tag in cases:
+        rc = lib.ozgpu_dgemm(ctx, 4, 6, 8, dp(a), lda, dp(b), ldb, dp(c), ldc, cfg._c(),
+                             ctypes.byref(plan), None)
+        if tag == "ok":
+            assert rc == 0
+        else:
+            assert rc == 1 and msg in lib.ozgpu_last_error().decode(), tag
+    rc = lib.ozgpu_dgemm(ctx, 4, 6, 8, None, 8, dp(b), 6, dp(c), 6, cfg._c(), ctypes.byref(plan),
+                         None)
+    assert rc == 1 and "null" in lib.ozgpu_last_error().decode()
+    rc = lib.ozgpu_dgemm_device(ctx, 4, 6, 8, None, 8, None, 6, None, 6, cfg._c(),
+                                ctypes.byref(plan), None, None, None)
+    assert rc == 1 and "null" in lib.ozgpu_last_error().decode()
+    # the next valid call is not poisoned by the rejected ones
+    assert lib.ozgpu_dgemm(ctx, 4, 6, 8, dp(a), 8, dp(b), 6, dp(c), 6, cfg._c(),
+                           ctypes.byref(plan), None) == 0
+    assert (c == 8.0).all()
+
+
+@pytest.mark.parametrize("shape", [(40, 30, 20), (600, 500, 400)])
+def test_rejected_inputs_leave_c_untouched(oz, shape):
+    """Inf / NaN / -0 inputs raise invalid_argument (scheme.cpp:223-225) and
+    the caller's C keeps its contents (unstaged path)."""
+    m, k, n = shape
+    cfg = oz.MmaConfig.int8_int32()
+    plan = oz.make_plan(cfg, k, 4, 4)
+    rng = np.random.default_rng(2)
+    a, b = uniform(m, k, rng), uniform(k, n, rng)
+    a[m // 2, k // 3] = np.nan
+    out = np.full((m, n), 7.25)
+    with pytest.raises(oz.InvalidArgument):
+        oz.multiply(a, b, cfg, plan, out=out)
+    assert (out == 7.25).all()

@@ -447,13 +447,16 @@ def test_split_k_tail_is_exact(oz, ref, m, n, k, slices, monkeypatch):
         assert bits_equal(got[r0:r1, c0:c1], exact[r0:r1, c0:c1])
 
 
-@pytest.mark.parametrize("stage_min", ["1", "0"])
-def test_pageable_staging_is_exact(oz, ref, stage_min, monkeypatch):
-    """Pageable host buffers are copied by host threads into the context's
-    pinned buffers before the GPU pipeline (ozgpu_dgemm); the result is
-    bitwise the unstaged one and matches the reference on sampled blocks."""
+@pytest.mark.parametrize("case", ["staged", "below_threshold", "staged_pipeline"])
+def test_pageable_staging_is_exact(oz, ref, case, monkeypatch):
+    """Pageable host buffers at or above OZGPU_STAGE_MIN bytes are copied by
+    host threads into the context's pinned buffers before the GPU pipeline
+    (ozgpu_dgemm); smaller products go unstaged.  Either way the result is
+    bitwise the unstaged one and matches the reference on sampled blocks --
+    incl. a product large enough for the blocked H2D / compute / D2H
+    pipeline (the default production route for pageable inputs)."""
     rng = np.random.default_rng(77)
-    m, k, n = 1100, 900, 1300
+    m, k, n = (2304, 1536, 2048) if case == "staged_pipeline" else (1100, 900, 1300)
     a = uniform(m, k, rng)
     b = random_matrix(k, n, rng, -9, 9, 0.02)
     cfg = oz.MmaConfig.int8_int32()
@@ -461,10 +464,53 @@ def test_pageable_staging_is_exact(oz, ref, stage_min, monkeypatch):
     monkeypatch.setenv("OZGPU_STAGE", "0")
     want = oz.multiply(a, b, cfg, plan).c
     monkeypatch.setenv("OZGPU_STAGE", "1")
-    monkeypatch.setenv("OZGPU_STAGE_MIN", stage_min)
+    total = 8 * (m * k + k * n + m * n)
+    monkeypatch.setenv("OZGPU_STAGE_MIN", str(total + 1) if case == "below_threshold" else "0")
     got = oz.multiply(a, b, cfg, plan).c
     assert bits_equal(got, want), mismatch_report(got, want)
     blocks = [(0, 8, 0, 8), (m - 8, m, n - 8, n)]
     exact, _ = ref.ref_multiply_blocks(a, b, 8, 7, blocks, 2)
     for r0, r1, c0, c1 in blocks:
         assert bits_equal(got[r0:r1, c0:c1], exact[r0:r1, c0:c1])
+
+
+def test_underflow_regime(oz, ref, po):
+    """Scaled products below 2^-1022 (scheme.cpp:205-215): the reference
+    rounds every pair term onto the subnormal grid inside ldexp before its
+    (otherwise exact) level sums, so it can miss RN(exact) by a few units of
+    2^-1074; the GPU computes the exact scheduled sum and rounds once.
+    Shown here: in the error-free regime (slices hold A and B exactly) the
+    GPU equals the exact product RN(AB) bit for bit -- as the C restatement of
+    the levelled-exact contract does -- and the reference stays within
+    (terms + 1) / 2 units of 2^-1074 of it; with truncating slices both stay
+    inside the a13 bound plus that underflow allowance."""
+    rng = np.random.default_rng(1)
+    cfg = oz.MmaConfig.int8_int32()
+    tiny = 2.0 ** -1074
+    m, k, n = 24, 40, 20
+    a = np.ldexp(rng.integers(-2**13, 2**13, size=(m, k)).astype(np.float64), -540)
+    b = np.ldexp(rng.integers(-2**13, 2**13, size=(k, n)).astype(np.float64), -540)
+    a[3] *= 2.0 ** 500  # a row of normal-range products next to subnormal ones
+    exact = ref.ref_exact_gemm(a, b)
+    assert (np.abs(exact[:3]) < 2.0 ** -1022).all()
+    for sa, sb, sched in [(4, 4, 0), (4, 4, 1), (3, 3, 0)]:
+        plan = oz.make_plan(cfg, k, sa, sb, oz.ScheduleKind(sched))
+        got = oz.multiply(a, b, cfg, plan).c
+        assert bits_equal(got, exact), mismatch_report(got, exact)
+        assert bits_equal(got, po.port_multiply_exact(a, b, sa, sb, sched))
+        want, diag = ref.ref_multiply(a, b, sa, sb, sched)
+        terms = diag[0]
+        assert (np.abs(want - exact) <= (terms + 1) * tiny / 2).all()
+    # truncating slices (uniform magnitudes, s = 2): both inside the bound
+    a2 = a * np.exp(rng.uniform(-3, 3, size=a.shape))
+    b2 = b * np.exp(rng.uniform(-3, 3, size=b.shape))
+    for sa, sb in [(2, 2), (3, 2)]:
+        plan = oz.make_plan(cfg, k, sa, sb)
+        got = oz.multiply(a2, b2, cfg, plan).c
+        want, diag = ref.ref_multiply(a2, b2, sa, sb)
+        rep = oz.error_bound(a2, b2, plan)
+        ex2 = ref.ref_exact_gemm(a2, b2)
+        allow = rep.bound + (diag[0] + 1) * tiny / 2
+        assert (np.abs(got - ex2) <= allow).all()
+        assert (np.abs(want - ex2) <= allow).all()
+        assert bits_equal(got, po.port_multiply_exact(a2, b2, sa, sb))
