@@ -191,6 +191,22 @@ int ozgpu_dgemm_axpby(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, double al
                       const double* a, int64_t lda, const double* b, int64_t ldb, double beta,
                       const double* c_in, int64_t ldc, double* d_out, int64_t ldd,
                       ozgpu_mma_config cfg, const ozgpu_plan* plan, ozgpu_diag* diag);
+/* The same multiply sharded over several contexts (one per GPU of the node,
+ * or several on one GPU): C is split into p_r x p_c blocks (p_r >= p_c,
+ * p_r * p_c = count, as square as possible: 1x1, 2x1, 2x2, 4x2); context r
+ * computes block (r / p_c, r % p_c) with the full k from its A row-panel and
+ * B column-panel, concurrently, each through its own blocked H2D / compute /
+ * D2H pipeline.  Bit-identical to ozgpu_dgemm (scales are per row of A and
+ * per column of B).  Errors: the first failing block's, in
+ * context order. */
+int ozgpu_dgemm_multi(ozgpu_ctx* const* ctxs, int count, int64_t m, int64_t n, int64_t k,
+                      const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
+                      int64_t ldc, ozgpu_mma_config cfg, const ozgpu_plan* plan,
+                      ozgpu_diag* diag);
+/* Contexts for a list of device slots (e.g. OZGPU_DEVICES=0,1,2,3): the first
+ * slot on a device gets its default context, repeated slots on the same
+ * device get further process-wide contexts of their own (cached). */
+int ozgpu_device_contexts(const int* devices, int count, ozgpu_ctx** out);
 /* Device-resident twin: a, b, c are device pointers; the work is enqueued on
  * `stream` (a cudaStream_t; NULL is the legacy default stream) and the call returns without
  * synchronising.  Input validity (Inf/NaN/-0, scheme.cpp:223-225) is

@@ -462,11 +462,33 @@ def scaling_profile(a, b, device: Optional[int] = None) -> ScalingProfile:
 # ------------------------------------------------------------------ GEMM
 
 
+_sig("ozgpu_dgemm_multi", ctypes.c_int, ctypes.POINTER(_P), ctypes.c_int, _I64, _I64, _I64, _DP,
+     _I64, _DP, _I64, _DP, _I64, _Cfg, ctypes.POINTER(_Plan), ctypes.POINTER(_Diag))
+_sig("ozgpu_device_contexts", ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.c_int,
+     ctypes.POINTER(_P))
+
+
+def _slots(devices) -> Optional[list]:
+    """Device slots for a sharded multiply: `devices` or $OZGPU_DEVICES."""
+    if devices is None:
+        env = os.environ.get("OZGPU_DEVICES", "")
+        devices = [int(v) for v in env.split(",") if v.strip()] if env else None
+    if devices is None or len(devices) < 2:
+        return None
+    arr = (ctypes.c_int * len(devices))(*devices)
+    ctxs = (_P * len(devices))()
+    _check(_lib.ozgpu_device_contexts(arr, len(devices), ctxs))
+    return ctxs
+
+
 def multiply(a, b, cfg: MmaConfig, plan: MultiplyPlan, device: Optional[int] = None,
-             out: Optional[np.ndarray] = None) -> MultiplyResult:
+             out: Optional[np.ndarray] = None, devices: Optional[List[int]] = None
+             ) -> MultiplyResult:
     """scheme.cpp:219-361 on the GPU (host arrays in, host array out).
 
-    `out` (optional) receives C in place, e.g. a pinned buffer."""
+    `out` (optional) receives C in place, e.g. a pinned buffer.  `devices`
+    (or $OZGPU_DEVICES, e.g. "0,1,2,3"): shard C in 2-D tiles over these GPUs
+    (ozgpu_dgemm_multi; a device may repeat: extra contexts on it)."""
     a, b = _f64(a), _f64(b)
     if a.shape[1] != b.shape[0]:
         raise InvalidArgument("multiply: shape mismatch")
@@ -480,8 +502,13 @@ def multiply(a, b, cfg: MmaConfig, plan: MultiplyPlan, device: Optional[int] = N
         c = np.empty((m, n), dtype=np.float64)
     d = _Diag()
     pc = plan._c()
-    _check(_lib.ozgpu_dgemm(_ctx(device), m, n, k, _dp(a), k, _dp(b), n, _dp(c), n, cfg._c(),
-                            ctypes.byref(pc), ctypes.byref(d)))
+    slots = _slots(devices) if device is None else None
+    if slots is not None:
+        _check(_lib.ozgpu_dgemm_multi(slots, len(slots), m, n, k, _dp(a), k, _dp(b), n, _dp(c),
+                                      n, cfg._c(), ctypes.byref(pc), ctypes.byref(d)))
+    else:
+        _check(_lib.ozgpu_dgemm(_ctx(device), m, n, k, _dp(a), k, _dp(b), n, _dp(c), n, cfg._c(),
+                                ctypes.byref(pc), ctypes.byref(d)))
     return MultiplyResult(c, Diagnostics._from_c(d))
 
 

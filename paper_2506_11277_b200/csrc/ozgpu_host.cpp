@@ -1890,6 +1890,93 @@ int ozgpu_split(ozgpu_ctx* ctx, int orientation, int64_t rows, int64_t cols, con
   });
 }
 
+int ozgpu_device_contexts(const int* devices, int count, ozgpu_ctx** out) {
+  return guarded([&] {
+    if (!devices || !out || count < 1) throw std::invalid_argument("device_contexts: bad arguments");
+    static std::mutex mu;
+    static std::map<std::pair<int, int>, ozgpu_ctx*> extra;  // (device, occurrence > 0)
+    std::lock_guard<std::mutex> lock(mu);
+    std::map<int, int> seen;
+    for (int s = 0; s < count; ++s) {
+      const int dev = devices[s];
+      const int occ = seen[dev]++;
+      if (occ == 0) {
+        out[s] = ozgpu_default_context(dev);
+        if (!out[s]) throw DeviceError(g_error);
+        continue;
+      }
+      auto& c = extra[{dev, occ}];
+      if (!c) {
+        ozgpu_ctx* made = nullptr;
+        if (ozgpu_create(dev, &made) != OZGPU_OK) throw DeviceError(g_error);
+        c = made;
+      }
+      out[s] = c;
+    }
+  });
+}
+
+// 2-D C-tile sharding of one host-pointer multiply over several contexts
+// (SURVEY.md 8e): context r computes C block (i, j) = divmod(r, p_c) with the
+// full k from its A row-panel and B column-panel, pulled from the caller's
+// host buffers over its own PCIe link by its own blocked pipeline.  Scales
+// are per row of A / column of B, so the blocks are bit-identical to the
+// single-context result; no device-to-device exchange is
+// needed because every panel starts on the host.
+int ozgpu_dgemm_multi(ozgpu_ctx* const* ctxs, int count, int64_t m, int64_t n, int64_t k,
+                      const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
+                      int64_t ldc, ozgpu_mma_config cfg, const ozgpu_plan* plan,
+                      ozgpu_diag* diag) {
+  int pr = 1, pc = 1;
+  int rc = guarded([&] {
+    if (!ctxs || count < 1) throw std::invalid_argument("multiply: no contexts");
+    for (int r = 0; r < count; ++r)
+      if (!ctxs[r]) throw std::invalid_argument("multiply: null context");
+    check_plan(plan);
+    check_operands("multiply", m, n, k, a, lda, b, ldb, c, ldc);
+    // p_r >= p_c, p_r * p_c == count, as square as possible (1x1, 2x1, 2x2, 4x2)
+    pr = count;
+    pc = 1;
+    for (int q = 1; q <= count; ++q)
+      if (count % q == 0 && count / q >= q) {
+        pr = count / q;
+        pc = q;
+      }
+  });
+  if (rc != OZGPU_OK) return rc;
+  if (count == 1 || m < pr || n < pc)  // nothing to shard (every block must be non-empty)
+    return ozgpu_dgemm(ctxs[0], m, n, k, a, lda, b, ldb, c, ldc, cfg, plan, diag);
+  auto split = [](int64_t len, int parts, int idx, int64_t& lo, int64_t& hi) {
+    const int64_t base = len / parts, rem = len % parts;
+    lo = idx * base + std::min<int64_t>(idx, rem);
+    hi = lo + base + (idx < rem ? 1 : 0);
+  };
+  std::vector<int> codes(count, OZGPU_OK);
+  std::vector<std::string> msgs(count);
+  std::vector<ozgpu_diag> diags(count);
+  std::vector<std::thread> pool;
+  for (int r = 0; r < count; ++r)
+    pool.emplace_back([&, r] {
+      int64_t r0, r1, c0, c1;
+      split(m, pr, r / pc, r0, r1);
+      split(n, pc, r % pc, c0, c1);
+      codes[r] = ozgpu_dgemm(ctxs[r], r1 - r0, c1 - c0, k, a + r0 * lda, lda, b + c0, ldb,
+                             c + r0 * ldc + c0, ldc, cfg, plan, &diags[r]);
+      if (codes[r] != OZGPU_OK) msgs[r] = g_error;  // thread-local: copy out
+    });
+  for (auto& th : pool) th.join();
+  for (int r = 0; r < count; ++r)
+    if (codes[r] != OZGPU_OK) {  // first failing block in rank order
+      g_error = msgs[r];
+      return codes[r];
+    }
+  return guarded([&] {
+    long long psi = 0;
+    for (const auto& d : diags) psi = std::max(psi, d.realized_psi);
+    if (diag) *diag = make_diag(*plan, cfg, m, n, k, psi);
+  });
+}
+
 int ozgpu_split_i8(ozgpu_ctx* ctx, int orientation, int64_t rows, int64_t cols, const double* x,
                    int64_t ldx, int width, int count, int mode, int8_t* slices_out, int64_t ld,
                    int* scales_out) {

@@ -12,6 +12,7 @@
 #include <cstring>
 #include <limits>
 #include <string>
+#include <vector>
 
 #include "ozgpu.h"
 #include "ozmul_b200/api.hpp"
@@ -24,6 +25,27 @@ ozgpu_ctx* ctx() {
   ozgpu_ctx* c = ozgpu_default_context(env ? std::atoi(env) : 0);
   if (!c) throw std::runtime_error(ozgpu_last_error());
   return c;
+}
+
+// $OZGPU_DEVICES (e.g. "0,1,2,3"): the device slots multiply() shards C over
+// (ozgpu_dgemm_multi); empty when unset or a single slot.
+std::vector<ozgpu_ctx*> shard_contexts() {
+  std::vector<ozgpu_ctx*> out;
+  const char* env = std::getenv("OZGPU_DEVICES");
+  if (!env || !*env) return out;
+  std::vector<int> devs;
+  for (const char* p = env; *p;) {
+    char* end = nullptr;
+    const long v = std::strtol(p, &end, 10);
+    if (end == p) throw std::invalid_argument("OZGPU_DEVICES: expected a comma-separated device list");
+    devs.push_back(static_cast<int>(v));
+    p = *end == ',' ? end + 1 : end;
+  }
+  if (devs.size() < 2) return out;
+  out.resize(devs.size());
+  if (ozgpu_device_contexts(devs.data(), static_cast<int>(devs.size()), out.data()) != OZGPU_OK)
+    throw std::runtime_error(ozgpu_last_error());
+  return out;
 }
 
 [[noreturn]] void rethrow(int rc, int acc_width = 31) {
@@ -429,6 +451,17 @@ MultiplyResult multiply(const Matrix& a, const Matrix& b, const MmaConfig& cfg,
   MultiplyResult r{Matrix(a.rows(), b.cols()), {}};
   ozgpu_plan p = to_c(plan);
   ozgpu_diag d{};
+  const std::vector<ozgpu_ctx*> slots = shard_contexts();
+  if (!slots.empty()) {  // 2-D C tiles over the listed GPUs (bit-identical)
+    check(ozgpu_dgemm_multi(slots.data(), static_cast<int>(slots.size()),
+                            static_cast<int64_t>(a.rows()), static_cast<int64_t>(b.cols()),
+                            static_cast<int64_t>(a.cols()), a.data(),
+                            static_cast<int64_t>(a.cols()), b.data(),
+                            static_cast<int64_t>(b.cols()), r.c.data(),
+                            static_cast<int64_t>(b.cols()), to_c(cfg), &p, &d));
+    r.diagnostics = from_c(d);
+    return r;
+  }
   check(ozgpu_dgemm(ctx(), static_cast<int64_t>(a.rows()), static_cast<int64_t>(b.cols()),
                     static_cast<int64_t>(a.cols()), a.data(), static_cast<int64_t>(a.cols()),
                     b.data(), static_cast<int64_t>(b.cols()), r.c.data(),

@@ -30,3 +30,17 @@ def mismatch_report(x, y, limit=5) -> str:
     bad = np.argwhere(x.view(np.uint64) != y.view(np.uint64))
     rows = [f"{tuple(i)}: got {x[tuple(i)]!r} want {y[tuple(i)]!r}" for i in bad[:limit]]
     return f"{len(bad)} mismatches; " + "; ".join(rows)
+
+
+def ref_full(ref, a, b, sa, sb, schedule=1, strategy=2, mode=0):
+    """The reference multiply() of the whole product, run as row blocks of C on
+    every host core (bit-identical to one call: each element's computation is
+    independent of the others and the scales are per row / column)."""
+    import os
+    m, n = a.shape[0], b.shape[1]
+    threads = os.cpu_count() or 4
+    parts = max(1, min(m, 2 * threads))
+    blocks = [(m * i // parts, m * (i + 1) // parts, 0, n) for i in range(parts)
+              if m * i // parts < m * (i + 1) // parts]
+    c, _ = ref.ref_multiply_blocks(a, b, sa, sb, blocks, threads, schedule, strategy, mode)
+    return c

@@ -6,7 +6,7 @@ import itertools
 import numpy as np
 import pytest
 
-from helpers import bits_equal, mismatch_report, random_matrix, uniform
+from helpers import bits_equal, mismatch_report, random_matrix, ref_full, uniform
 
 pytestmark = pytest.mark.gpu
 
@@ -249,6 +249,26 @@ GEMM_VARIANTS = {
 }
 
 
+_VARIANT_CASES = []
+
+
+def _variant_cases(ref):
+    """Inputs and reference results shared by every GEMM variant (computed
+    once: the reference's scalar loop dominates the test time)."""
+    if not _VARIANT_CASES:
+        rng = np.random.default_rng(77)
+        for (m, k, n) in [(128, 256, 256), (300, 500, 700), (520, 128, 260)]:
+            a = uniform(m, k, rng)
+            b = random_matrix(k, n, rng, -30, 30, 0.02)
+            for (sa, sb), sched in [((4, 4), 1), ((13, 12), 1), ((16, 17), 1), ((6, 7), 0)]:
+                _VARIANT_CASES.append((a, b, sa, sb, sched, ref_full(ref, a, b, sa, sb, sched)))
+        a = uniform(256, 384, rng)
+        b = uniform(384, 512, rng)
+        c = uniform(256, 512, rng)
+        _VARIANT_CASES.append((a, b, c, ref.ref_multiply_axpby(1.5, a, b, -0.25, c, 7, 7)))
+    return _VARIANT_CASES
+
+
 @pytest.mark.parametrize("variant", sorted(GEMM_VARIANTS))
 def test_gemm_variants_match_reference(oz, ref, variant, monkeypatch):
     """Every GEMM variant -- the CTA-pair (cta_group::2) kernel with and
@@ -256,25 +276,18 @@ def test_gemm_variants_match_reference(oz, ref, variant, monkeypatch):
     1-CTA kernels, equal-length chunk bins on / off, the fused W-word and
     folded-combine epilogues, both exact combine kernels -- is bit-exact,
     incl. ragged tiles and 3-word exact values."""
+    cases = _variant_cases(ref)
     for key, val in GEMM_VARIANTS[variant].items():
         monkeypatch.setenv(key, val)
-    rng = np.random.default_rng(77)
     cfg = oz.MmaConfig.int8_int32()
-    for (m, k, n) in [(128, 256, 256), (300, 500, 700), (520, 128, 260)]:
-        a = uniform(m, k, rng)
-        b = random_matrix(k, n, rng, -30, 30, 0.02)
-        for (sa, sb), sched in [((4, 4), 1), ((13, 12), 1), ((16, 17), 1), ((6, 7), 0)]:
-            plan = oz.make_plan(cfg, k, sa, sb, oz.ScheduleKind(sched))
-            got = oz.multiply(a, b, cfg, plan).c
-            want, _ = ref.ref_multiply(a, b, sa, sb, sched)
-            assert bits_equal(got, want), (m, k, n, sa, sb, mismatch_report(got, want))
+    for a, b, sa, sb, sched, want in cases[:-1]:
+        plan = oz.make_plan(cfg, a.shape[1], sa, sb, oz.ScheduleKind(sched))
+        got = oz.multiply(a, b, cfg, plan).c
+        assert bits_equal(got, want), (a.shape, b.shape, sa, sb, mismatch_report(got, want))
     # axpby through the fused epilogue
-    a = uniform(256, 384, rng)
-    b = uniform(384, 512, rng)
-    c = uniform(256, 512, rng)
+    a, b, c, want = cases[-1]
     plan = oz.make_plan(cfg, 384, 7, 7)
     got = oz.multiply_axpby(1.5, a, b, -0.25, c, cfg, plan).c
-    want = ref.ref_multiply_axpby(1.5, a, b, -0.25, c, 7, 7)
     assert bits_equal(got, want)
 
 
@@ -398,8 +411,8 @@ def test_device_path_graph_replay_is_exact(oz, ref, monkeypatch):
     A = torch.from_numpy(a1).to(dev)
     B = torch.from_numpy(b1).to(dev)
     C = torch.empty(m, n, dtype=torch.float64, device=dev)
-    want1, _ = ref.ref_multiply(a1, b1, 7, 6, 1)
-    want2, _ = ref.ref_multiply(a2, b1, 7, 6, 1)
+    want1 = ref_full(ref, a1, b1, 7, 6)
+    want2 = ref_full(ref, a2, b1, 7, 6)
 
     def run():
         oz.multiply_device(m, n, k, A.data_ptr(), k, B.data_ptr(), n, C.data_ptr(), n, cfg, plan,
