@@ -166,7 +166,7 @@ struct ozgpu_ctx {
   };
   std::map<std::string, GraphEntry> graphs;
   GraphEntry* capturing = nullptr;
-  ozgpu::DevBuf aux, counters, sync;
+  ozgpu::DevBuf aux, counters, sync, qwork;
   // row-blocked H2D / compute / D2H pipeline of ozgpu_dgemm
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
   // B's slicing runs on a forked stream, joined before the GEMM
@@ -224,6 +224,31 @@ void init_ctx(ozgpu_ctx* ctx, int device) {
   if (!fn || q != cudaDriverEntryPointSuccess)
     throw DeviceError("cuTensorMapEncodeTiled unavailable from the driver");
   ctx->encode = reinterpret_cast<EncodeTiledFn>(fn);
+}
+
+// The one-launch queue slicer (launch_slice_queue, OZGPU_SLICE_QUEUE=1) for
+// truncate-mode int8 operands.  Opt-in: measured on B200 it reads A and B
+// 1.67x instead of 2x from DRAM (the slice pass's L2 re-reads still miss 65%
+// with ~16 MB panels while the 1.6 GB of slice writes stream through L2) and
+// is issue-bound like the two-kernel path, 1.11 vs 0.97 ms at 8192^2 (12,12)
+// and 4.1 vs 3.4 ms at 16384^2 (13,12) inside the power-capped step
+// (DESIGN.md 4).
+bool use_slice_queue(int mode, int t, int64_t ld) {
+  if (mode != 0 || t < 1 || t > 7 || ld % kKPad) return false;
+  const char* env = std::getenv("OZGPU_SLICE_QUEUE");
+  return env && std::string(env) == "1";
+}
+
+void upload_table(ozgpu_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st);
+
+// UploadFn for the queue slicer's segment table
+void upload_cb(void* user, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  upload_table(static_cast<ozgpu_ctx*>(user), dst, src, bytes, st);
+}
+
+int* queue_work(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t ld) {
+  return static_cast<int*>(
+      ctx->qwork.get(sizeof(int) * static_cast<size_t>(slice_queue_work_ints(m, n, k, ld))));
 }
 
 // Orders this call's use of the context workspace after every earlier
@@ -612,6 +637,16 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
     auto* colmax = static_cast<unsigned long long*>(ctx->colmax.get(8 * (n + 1)));
     int* status = dev_status ? dev_status : static_cast<int*>(ctx->status.get(sizeof(int)));
     OZ_CUDA(cudaMemsetAsync(status, 0, sizeof(int), st));
+    if (use_slice_queue(p.mode, t, ld)) {
+      // both operands in one launch, each read once from DRAM
+      OZ_CUDA(launch_slice_queue(da, lda, m, db, ldb, n, k, ld, t, sa, sb, wa, 0, wb, 0, wqa, wqb,
+                                 colmax, queue_work(ctx, m, n, k, ld), status, upload_cb, ctx, st,
+                                 &launches));
+      slA = wa;
+      slB = wb;
+      qa = wqa;
+      qb = wqb;
+    } else {
     // A's and B's slicing are independent: B's runs on a forked stream so
     // the two HBM-bound chains overlap (their tails and the short memsets
     // hide each other); joined before the GEMM.  OZGPU_SLICE_FORK=0: serial.
@@ -642,6 +677,7 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
     slB = wb;
     qa = wqa;
     qb = wqb;
+    }
   }
   if (ctx->timing) OZ_CUDA(cudaEventRecord(ev[1], st));
 
@@ -1246,10 +1282,19 @@ void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const
       for (size_t i = 1; i < nr; ++i) copy_a(i);
     }
     int64_t launches = 0;
+    const bool queue = use_slice_queue(p.mode, t, kp);
+    int* qwork = queue ? queue_work(ctx, m, n, k, kp) : nullptr;
     auto slice_a = [&](size_t i) {
       OZ_CUDA(cudaStreamWaitEvent(st, a_in[i], 0));
-      OZ_CUDA(launch_slice_rows(da + rb[i] * k, k, rb[i + 1] - rb[i], k, kp, t, p.slices_a, p.mode,
-                                slA + rb[i] * kp, 0, qa + rb[i], status, st, &launches, m * kp));
+      if (queue)
+        OZ_CUDA(launch_slice_queue(da + rb[i] * k, k, rb[i + 1] - rb[i], nullptr, 0, 0, k, kp, t,
+                                   p.slices_a, 0, slA + rb[i] * kp, m * kp, nullptr, 0,
+                                   qa + rb[i], nullptr, nullptr, qwork, status, upload_cb, ctx, st,
+                                   &launches));
+      else
+        OZ_CUDA(launch_slice_rows(da + rb[i] * k, k, rb[i + 1] - rb[i], k, kp, t, p.slices_a,
+                                  p.mode, slA + rb[i] * kp, 0, qa + rb[i], status, st, &launches,
+                                  m * kp));
       mark("slice A" + std::to_string(i), st);
     };
     auto block = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1) {
@@ -1270,9 +1315,14 @@ void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const
     auto slice_b = [&](size_t j) {
       const int64_t nj = cb[j + 1] - cb[j];
       OZ_CUDA(cudaStreamWaitEvent(st, b_in[j], 0));
-      OZ_CUDA(launch_slice_cols(db + k * cb[j], nj, k, nj, kp, t, p.slices_b, p.mode,
-                                slB + cb[j] * kp, 0, qb + cb[j], colmax + cb[j], status, st,
-                                &launches, n * kp));
+      if (queue)
+        OZ_CUDA(launch_slice_queue(nullptr, 0, 0, db + k * cb[j], nj, nj, k, kp, t, 0, p.slices_b,
+                                   nullptr, 0, slB + cb[j] * kp, n * kp, nullptr, qb + cb[j],
+                                   colmax + cb[j], qwork, status, upload_cb, ctx, st, &launches));
+      else
+        OZ_CUDA(launch_slice_cols(db + k * cb[j], nj, k, nj, kp, t, p.slices_b, p.mode,
+                                  slB + cb[j] * kp, 0, qb + cb[j], colmax + cb[j], status, st,
+                                  &launches, n * kp));
     };
     if (rect) {
       size_t na = 0, nbp = 0;  // A blocks / B panels sliced so far
@@ -2008,11 +2058,21 @@ int ozgpu_split_i8(ozgpu_ctx* ctx, int orientation, int64_t rows, int64_t cols, 
     int8_t* out = static_cast<int8_t*>(ctx->slices_a.get(bytes + 1));
     int* scales = static_cast<int*>(ctx->qa.get(sizeof(int) * (blocks + 1)));
     // exactly the launches run_multiply makes for its operands
-    if (orientation == 0) {
+    auto* colmax = static_cast<unsigned long long*>(ctx->colmax.get(8 * (cols + 1)));
+    if (use_slice_queue(mode, width, ld)) {
+      int* qw = queue_work(ctx, rows, cols, len, ld);
+      if (orientation == 0)
+        OZ_CUDA(launch_slice_queue(dx, cols, rows, nullptr, 0, 0, cols, ld, width, count, 0, out,
+                                   0, nullptr, 0, scales, nullptr, nullptr, qw, status, upload_cb,
+                                   ctx, st, &launches));
+      else
+        OZ_CUDA(launch_slice_queue(nullptr, 0, 0, dx, cols, cols, rows, ld, width, 0, count,
+                                   nullptr, 0, out, 0, nullptr, scales, colmax, qw, status, upload_cb,
+                                   ctx, st, &launches));
+    } else if (orientation == 0) {
       OZ_CUDA(launch_slice_rows(dx, cols, rows, cols, ld, width, count, mode, out, 0, scales,
                                 status, st, &launches));
     } else {
-      auto* colmax = static_cast<unsigned long long*>(ctx->colmax.get(8 * (cols + 1)));
       OZ_CUDA(launch_slice_cols(dx, cols, rows, cols, ld, width, count, mode, out, 0, scales,
                                 colmax, status, st, &launches));
     }

@@ -108,6 +108,20 @@ cudaError_t launch_slice_cols(const double* b, int64_t ldb, int64_t k, int64_t n
                               int width, int count, int mode, void* out, int out_is_i64,
                               int* scales, unsigned long long* colmax, int* status,
                               cudaStream_t st, int64_t* launches, int64_t plane = 0);
+// One persistent launch slicing A (rows) and / or B (columns) in truncate
+// mode at width <= 7 into int8, reading each operand once from DRAM (ordered
+// work queue over L2-sized panels).  a or b may be null (one operand only).
+// work: slice_queue_work_ints(m, n, k, kp) ints of device scratch.
+// upload copies a small host table to the device on `st` (graph-capture safe).
+using UploadFn = void (*)(void* user, void* dst, const void* src, size_t bytes, cudaStream_t st);
+int slice_queue_work_ints(int64_t m, int64_t n, int64_t k, int64_t kp);
+cudaError_t launch_slice_queue(const double* a, int64_t lda, int64_t m, const double* b,
+                               int64_t ldb, int64_t n, int64_t k, int64_t kp, int width,
+                               int count_a, int count_b, int8_t* out_a, int64_t plane_a,
+                               int8_t* out_b, int64_t plane_b, int* scales_a, int* scales_b,
+                               unsigned long long* colmax, int* work, int* status,
+                               UploadFn upload, void* upload_user, cudaStream_t st,
+                               int64_t* launches);
 cudaError_t launch_gemm_i8(const CUtensorMap* tma, const CUtensorMap* tmb, const GemmArgs& args,
                            int num_sms, cudaStream_t st, int64_t* launches);
 cudaError_t launch_gemm_i8_mc(const CUtensorMap* tma, const CUtensorMap* tmb_half,

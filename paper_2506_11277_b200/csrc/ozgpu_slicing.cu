@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <string>
+#include <vector>
 
 #include "ozgpu_internal.h"
 #include "ozgpu_numeric.h"
@@ -185,7 +186,7 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(
 // truncate mode (extract_field, slicing.cpp:35-45).
 // ----------------------------------------------------------------------------
 
-template <int T>
+template <int T, bool CS = false>
 __device__ __forceinline__ void emit8_trunc_i8(const double (&v)[8], int q, int count,
                                                int8_t* __restrict__ out, int64_t plane,
                                                int64_t off) {
@@ -236,7 +237,10 @@ __device__ __forceinline__ void emit8_trunc_i8(const double (&v)[8], int q, int 
       }
       lo = __vsub4(lo ^ neg_lo, neg_lo);
       hi = __vsub4(hi ^ neg_hi, neg_hi);
-      *reinterpret_cast<uint2*>(out + l * plane + off) = make_uint2(lo, hi);
+      if constexpr (CS)  // streaming store: keep L2 for the panels awaiting their slice pass
+        __stcs(reinterpret_cast<uint2*>(out + l * plane + off), make_uint2(lo, hi));
+      else
+        *reinterpret_cast<uint2*>(out + l * plane + off) = make_uint2(lo, hi);
     }
   }
 }
@@ -389,6 +393,399 @@ __global__ void __launch_bounds__(256) slice_cols_fast_kernel(
     }
     emit8_trunc_i8<T>(v, q, count, out, plane, col * kp + kk);
   }
+}
+
+// ----------------------------------------------------------------------------
+// One launch slicing both operands through an ordered work queue.
+//
+// The block scale of a row of A (a column of B) depends on the whole row
+// (column), so the two-kernel path above reads each operand twice from DRAM.
+// Here each operand is cut into panels of ~16 MB and one persistent launch
+// takes work items from a global ticket in a fixed order
+//     max(P0), max(P1), slice(P0), max(P2), slice(P1), ..., slice(P_last)
+// (the panels of A, then those of B).  A slice item of panel p first waits
+// until every max item of p has finished (a per-panel counter); tickets are
+// handed out in order and max items never wait, so a wait always ends.  The
+// slice pass re-reads a panel about one panel-time after its max pass, from
+// L2, so DRAM reads each operand once.
+// ----------------------------------------------------------------------------
+
+struct SliceQueueOp {
+  const double* x;  // A: blocks x len rows (ldx); B: len x blocks (ldx)
+  int64_t ldx;
+  int64_t blocks;   // rows of A / columns of B
+  int64_t len;      // k
+  int64_t kp;       // output row stride (multiple of 128), zero-filled past len
+  int64_t plane;
+  int8_t* out;
+  int* scales;
+  unsigned long long* colmax;  // B: zeroed before the launch
+  int count;
+  int panel;        // blocks per panel (A: multiple of 8; B: multiple of 32)
+  int npanels;
+  int max_items;    // per panel
+  int slice_items;  // per panel
+  int rb;           // B: rows per max item
+  int cw;           // B: columns per max item (32..256, divides 256 and the panel)
+  int vec;          // A: 16-byte loads are legal
+};
+
+struct SliceQueueArgs {
+  SliceQueueOp op[2];  // 0 = A (rows), 1 = B (columns)
+  int* ticket;         // ticket[0]: next item; ticket[1 + g]: finished max items of panel g
+  const int* seg_start;  // nseg + 1 ascending ticket offsets of the queue's segments
+  const int* seg_info;   // per segment: 2 * panel + (1 = slice items, 0 = max items)
+  int nseg;
+  int* status;
+  int total;
+};
+
+constexpr int kQueueGroups = 2048;  // A slice item: 2048 groups of 8 entries (128 KB of A)
+
+__device__ __forceinline__ int q_ld_acquire(const int* ptr) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
+  return v;
+}
+
+// ticket -> (is_slice, global panel g, item within the panel's max / slice set)
+__device__ __forceinline__ void queue_item(const SliceQueueArgs& p, int t, int& is_slice, int& g,
+                                           int& item) {
+  int lo = 0, hi = p.nseg - 1;  // last segment with start <= t
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(p.seg_start + mid) <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  const int info = __ldg(p.seg_info + lo);
+  is_slice = info & 1;
+  g = info >> 1;
+  item = t - __ldg(p.seg_start + lo);
+}
+
+template <int T>
+__global__ void __launch_bounds__(256, 3) slice_queue_kernel(const SliceQueueArgs p) {
+  constexpr int TK = 128, TN = 32, STRIDE = TK + 2;
+  __shared__ __align__(16) double tile[TN * STRIDE];
+  __shared__ int s_ticket;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (;;) {
+    if (tid == 0) s_ticket = atomicAdd(p.ticket, 1);
+    __syncthreads();
+    const int t = s_ticket;
+    __syncthreads();  // s_ticket is rewritten next round
+    if (t >= p.total) return;
+    int is_slice, g, item;
+    queue_item(p, t, is_slice, g, item);
+    const int o = g < p.op[0].npanels ? 0 : 1;
+    const SliceQueueOp& op = p.op[o];
+    const int pg = o == 0 ? g : g - p.op[0].npanels;  // panel within the operand
+    const int64_t b0 = static_cast<int64_t>(pg) * op.panel;
+    const int64_t b1 = b0 + op.panel < op.blocks ? b0 + op.panel : op.blocks;
+    if (!is_slice) {
+      if (o == 0) {
+        // ---- max of 8 rows of A, one warp per row (16-byte loads) ----
+        const int64_t row = b0 + static_cast<int64_t>(item) * 8 + warp;
+        if (row < b1) {
+          const double* ar = op.x + row * op.ldx;
+          unsigned long long mx = 0;
+          int bad = 0;
+          int64_t j = 0;
+          if (op.vec) {
+            const double2* a2 = reinterpret_cast<const double2*>(ar);
+            const int64_t k2 = op.len / 2;
+            int64_t u = lane;
+            for (; u + 224 < k2; u += 256) {
+              double2 x[8];
+#pragma unroll
+              for (int q = 0; q < 8; ++q) x[q] = __ldcg(a2 + u + 32 * q);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                bad |= dirty(x[q].x) | dirty(x[q].y);
+                const unsigned long long c0 = abs_bits(x[q].x), c1 = abs_bits(x[q].y);
+                mx = c0 > mx ? c0 : mx;
+                mx = c1 > mx ? c1 : mx;
+              }
+            }
+            for (; u < k2; u += 32) {
+              const double2 x = __ldcg(a2 + u);
+              bad |= dirty(x.x) | dirty(x.y);
+              const unsigned long long c0 = abs_bits(x.x), c1 = abs_bits(x.y);
+              mx = c0 > mx ? c0 : mx;
+              mx = c1 > mx ? c1 : mx;
+            }
+            j = 2 * k2 + lane;
+          } else {
+            j = lane;
+          }
+          for (; j < op.len; j += 32) {
+            const double x = __ldcg(ar + j);
+            bad |= dirty(x);
+            const unsigned long long c = abs_bits(x);
+            mx = c > mx ? c : mx;
+          }
+#pragma unroll
+          for (int sft = 16; sft; sft >>= 1) {
+            const unsigned long long u2 = __shfl_xor_sync(0xFFFFFFFFu, mx, sft);
+            mx = u2 > mx ? u2 : mx;
+          }
+          bad = __reduce_or_sync(0xFFFFFFFFu, bad);
+          if (lane == 0) {
+            if (bad) atomicOr(p.status, bad);
+            op.scales[row] = scale_from_maxbits(mx);
+          }
+        }
+      } else {
+        // ---- column max over rb rows x cw columns of B ----
+        const int subs = op.panel / op.cw;
+        const int sub = item % subs, rc = item / subs;
+        const int col_in = tid % op.cw, rg = tid / op.cw, ngroups = 256 / op.cw;
+        const int64_t col = b0 + static_cast<int64_t>(sub) * op.cw + col_in;
+        const int64_t r0 = static_cast<int64_t>(rc) * op.rb;
+        const int64_t r1 = r0 + op.rb < op.len ? r0 + op.rb : op.len;
+        if (col < b1) {
+          unsigned long long mx = 0;
+          int bad = 0;
+          int64_t r = r0 + rg;
+          for (; r + 7 * ngroups < r1; r += 8 * ngroups) {
+            double x[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) x[q] = __ldcg(op.x + (r + q * ngroups) * op.ldx + col);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              bad |= dirty(x[q]);
+              const unsigned long long c = abs_bits(x[q]);
+              mx = c > mx ? c : mx;
+            }
+          }
+          for (; r < r1; r += ngroups) {
+            const double x = __ldcg(op.x + r * op.ldx + col);
+            bad |= dirty(x);
+            const unsigned long long c = abs_bits(x);
+            mx = c > mx ? c : mx;
+          }
+          if (bad) atomicOr(p.status, bad);
+          if (mx) atomicMax(op.colmax + col, mx);
+        }
+      }
+      __syncthreads();  // every thread's scale / colmax update precedes the release
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(p.ticket + 1 + g, 1);
+      }
+      continue;
+    }
+    // slice item: wait for the panel's scales
+    if (tid == 0)
+      while (q_ld_acquire(p.ticket + 1 + g) < op.max_items) __nanosleep(64);
+    __syncthreads();
+    if (o == 0) {
+      // ---- slice rows of A: 2048 groups of 8 entries, 8 per thread ----
+      const int64_t gpr = op.kp / 8;
+      const int64_t e_end0 = (b1 - b0) * gpr;
+      const int64_t e0 = static_cast<int64_t>(item) * kQueueGroups;
+      const int64_t e1 = e0 + kQueueGroups < e_end0 ? e0 + kQueueGroups : e_end0;
+      for (int64_t e = e0 + tid; e < e1; e += 256) {
+        const int64_t row = b0 + e / gpr, j0 = (e % gpr) * 8;
+        const double* ar = op.x + row * op.ldx;
+        double v[8];
+        if (op.vec && j0 + 8 <= op.len) {
+          const double2* p2 = reinterpret_cast<const double2*>(ar + j0);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const double2 t2 = __ldcs(p2 + u);  // last use of A: evict first
+            v[2 * u] = t2.x;
+            v[2 * u + 1] = t2.y;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) v[q] = j0 + q < op.len ? __ldcs(ar + j0 + q) : 0.0;
+        }
+        emit8_trunc_i8<T, true>(v, __ldcg(op.scales + row), op.count, op.out, op.plane,
+                                row * op.kp + j0);
+      }
+    } else {
+      // ---- slice a 128 (k) x 32 (n) tile of B, transposed through smem ----
+      const int ktiles = static_cast<int>(op.kp / TK);
+      const int kt = item % ktiles, nt = item / ktiles;
+      const int64_t k0 = static_cast<int64_t>(kt) * TK;
+      const int64_t n0 = b0 + static_cast<int64_t>(nt) * TN;
+      auto pos = [](int c, int r) {
+        int u = r >> 1;
+        return c * STRIDE + ((u ^ ((u >> 2) & 7)) << 1) + (r & 1);
+      };
+      {
+        double v[16];
+        const int64_t c = n0 + lane;
+        const bool cok = c < b1;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = 2 * (warp + 8 * i);
+          const int64_t kr = k0 + r;
+          v[2 * i] = (kr < op.len && cok) ? __ldcs(op.x + kr * op.ldx + c) : 0.0;
+          v[2 * i + 1] = (kr + 1 < op.len && cok) ? __ldcs(op.x + (kr + 1) * op.ldx + c) : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = 2 * (warp + 8 * i);
+          *reinterpret_cast<double2*>(&tile[pos(lane, r)]) = make_double2(v[2 * i], v[2 * i + 1]);
+        }
+      }
+      if (kt == 0 && tid < TN && n0 + tid < b1)
+        op.scales[n0 + tid] = scale_from_maxbits(__ldcg(op.colmax + n0 + tid));
+      __syncthreads();
+      for (int it = tid; it < TN * (TK / 8); it += 256) {
+        const int c = it / (TK / 8), gq = it % (TK / 8);
+        const int64_t col = n0 + c, kk = k0 + gq * 8;
+        if (col >= b1) continue;
+        const int q = scale_from_maxbits(__ldcg(op.colmax + col));
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double2 t2 = *reinterpret_cast<const double2*>(&tile[pos(c, gq * 8 + 2 * u)]);
+          v[2 * u] = t2.x;
+          v[2 * u + 1] = t2.y;
+        }
+        emit8_trunc_i8<T, true>(v, q, op.count, op.out, op.plane, col * op.kp + kk);
+      }
+      __syncthreads();  // the tile is refilled by the next item
+    }
+  }
+}
+
+// Panel geometry of the queue launch (host side).  ~16 MB panels
+// (OZGPU_SLICE_PANEL_MB): two of them in flight stay well inside L2.
+static void plan_queue_op(SliceQueueOp& q, bool rows) {
+  double mb = 16.0;
+  if (const char* env = std::getenv("OZGPU_SLICE_PANEL_MB")) mb = std::max(1.0, std::atof(env));
+  const int64_t per = static_cast<int64_t>(mb * 1048576.0 / (8.0 * std::max<int64_t>(q.len, 1)));
+  if (q.blocks <= 0) {
+    q.npanels = 0, q.max_items = 0, q.slice_items = 0, q.panel = 8;
+    return;
+  }
+  if (rows) {
+    int64_t pr = std::max<int64_t>(8, per / 8 * 8);
+    pr = std::min<int64_t>(pr, (q.blocks + 7) / 8 * 8);
+    q.panel = static_cast<int>(pr);
+    q.max_items = static_cast<int>(pr / 8);
+    q.slice_items = static_cast<int>((pr * (q.kp / 8) + kQueueGroups - 1) / kQueueGroups);
+  } else {
+    int64_t pc = std::max<int64_t>(32, per / 32 * 32);
+    pc = std::min<int64_t>(pc, (q.blocks + 31) / 32 * 32);
+    int cw;
+    if (pc >= 256) {
+      pc = pc / 256 * 256;
+      cw = 256;
+    } else {
+      cw = pc >= 128 ? 128 : pc >= 64 ? 64 : 32;
+      pc = cw;
+    }
+    q.panel = static_cast<int>(pc);
+    q.cw = cw;
+    q.rb = static_cast<int>(std::max<int64_t>(8, 32768 / cw));  // ~256 KB of B per max item
+    q.max_items = static_cast<int>((pc / cw) * ((q.len + q.rb - 1) / q.rb));
+    q.slice_items = static_cast<int>((q.kp / 128) * (pc / 32));
+  }
+  q.npanels = static_cast<int>((q.blocks + q.panel - 1) / q.panel);
+}
+
+int slice_queue_work_ints(int64_t m, int64_t n, int64_t k, int64_t kp) {
+  SliceQueueOp a{}, b{};
+  a.blocks = m, a.len = k, a.kp = kp;
+  b.blocks = n, b.len = k, b.kp = kp;
+  plan_queue_op(a, true);
+  plan_queue_op(b, false);
+  const int P = a.npanels + b.npanels;
+  return 1 + P + (2 * P + 1) + 2 * P;  // counters, segment starts, segment infos
+}
+
+template <int T>
+static void launch_queue_t(const SliceQueueArgs& qa, int grid, cudaStream_t st) {
+  slice_queue_kernel<T><<<grid, 256, 0, st>>>(qa);
+}
+
+cudaError_t launch_slice_queue(const double* a, int64_t lda, int64_t m, const double* b,
+                               int64_t ldb, int64_t n, int64_t k, int64_t kp, int width,
+                               int count_a, int count_b, int8_t* out_a, int64_t plane_a,
+                               int8_t* out_b, int64_t plane_b, int* scales_a, int* scales_b,
+                               unsigned long long* colmax, int* work, int* status,
+                               UploadFn upload, void* upload_user, cudaStream_t st,
+                               int64_t* launches) {
+  SliceQueueArgs q{};
+  SliceQueueOp& A = q.op[0];
+  SliceQueueOp& B = q.op[1];
+  A.x = a, A.ldx = lda, A.blocks = a ? m : 0, A.len = k, A.kp = kp;
+  A.plane = plane_a ? plane_a : m * kp, A.out = out_a, A.scales = scales_a, A.count = count_a;
+  A.vec = (reinterpret_cast<uintptr_t>(a) & 15) == 0 && (lda & 1) == 0;
+  B.x = b, B.ldx = ldb, B.blocks = b ? n : 0, B.len = k, B.kp = kp;
+  B.plane = plane_b ? plane_b : n * kp, B.out = out_b, B.scales = scales_b, B.colmax = colmax;
+  B.count = count_b;
+  plan_queue_op(A, true);
+  plan_queue_op(B, false);
+  const int P = A.npanels + B.npanels;
+  if (P == 0) return cudaSuccess;
+  // Queue order with a lookahead of L panels: max(0..L-1), then max(h),
+  // slice(h - L) for h = L..P-1, then the last L slices.  L is sized so that
+  // a panel's slice items are handed out only after about one full wave of
+  // other items followed its max items (OZGPU_SLICE_LOOKAHEAD).
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int ctas = 3 * sms;
+  auto mi = [&](int g) { return g < A.npanels ? A.max_items : B.max_items; };
+  auto si = [&](int g) { return g < A.npanels ? A.slice_items : B.slice_items; };
+  int L = 0;
+  if (const char* env = std::getenv("OZGPU_SLICE_LOOKAHEAD")) {
+    L = std::max(1, std::atoi(env));
+  } else {
+    const int per = std::max(1, std::min(A.npanels ? A.max_items + A.slice_items : 1 << 30,
+                                         B.npanels ? B.max_items + B.slice_items : 1 << 30));
+    L = std::max(1, (ctas + per - 1) / per);
+  }
+  L = std::min(L, P);
+  std::vector<int> table;  // [nseg + 1 starts][nseg infos]
+  std::vector<int> starts, infos;
+  int pos = 0;
+  auto seg = [&](int g, int kind) {
+    const int cnt = kind ? si(g) : mi(g);
+    if (cnt <= 0) return;
+    starts.push_back(pos);
+    infos.push_back(2 * g + kind);
+    pos += cnt;
+  };
+  for (int h = 0; h < L; ++h) seg(h, 0);
+  for (int h = L; h < P; ++h) {
+    seg(h, 0);
+    seg(h - L, 1);
+  }
+  for (int h = P - L; h < P; ++h) seg(h, 1);
+  const int nseg = static_cast<int>(infos.size());
+  starts.push_back(pos);
+  table.insert(table.end(), starts.begin(), starts.end());
+  table.insert(table.end(), infos.begin(), infos.end());
+  q.total = pos;
+  q.ticket = work;
+  q.seg_start = work + 1 + P;
+  q.seg_info = work + 1 + P + nseg + 1;
+  q.nseg = nseg;
+  q.status = status;
+  upload(upload_user, work + 1 + P, table.data(), sizeof(int) * table.size(), st);
+  cudaError_t e = cudaMemsetAsync(work, 0, sizeof(int) * (1 + P), st);
+  if (e == cudaSuccess && B.blocks > 0)
+    e = cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * n, st);
+  if (e != cudaSuccess) return e;
+  const int grid = std::min(q.total, ctas);
+  switch (width) {
+    case 7: launch_queue_t<7>(q, grid, st); break;
+    case 6: launch_queue_t<6>(q, grid, st); break;
+    case 5: launch_queue_t<5>(q, grid, st); break;
+    case 4: launch_queue_t<4>(q, grid, st); break;
+    case 3: launch_queue_t<3>(q, grid, st); break;
+    case 2: launch_queue_t<2>(q, grid, st); break;
+    default: launch_queue_t<1>(q, grid, st); break;
+  }
+  ++*launches;
+  return cudaGetLastError();
 }
 
 static inline int grid_for(int64_t work, int per_block, int cap = 148 * 16) {

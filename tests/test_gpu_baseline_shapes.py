@@ -105,7 +105,9 @@ def test_configs2_kappa_d_estimator_choice(oz, ref, kappa_d):
     assert (sel2.slices_a, sel2.slices_b) == (wsel2["slices_a"], wsel2["slices_b"]) == (17, 17)
 
 
-def test_configs2_kappa_d_slices(oz, ref, kappa_d):
+@pytest.mark.parametrize("queue", ["0", "1"])
+def test_configs2_kappa_d_slices(oz, ref, kappa_d, queue, monkeypatch):
+    monkeypatch.setenv("OZGPU_SLICE_QUEUE", queue)  # two-kernel (default) / one-launch queue slicer
     a, b = kappa_d
     sample = [0, 1, 777, 2048, 4000, 4095]
     _check_slices_rows(oz, ref, a, 16, sample)

@@ -229,7 +229,7 @@ def test_native_kernels_launched(oz):
     cfg = oz.MmaConfig.int8_int32()
     before = oz.kernel_launches()
     oz.multiply(np.ones((8, 8)), np.ones((8, 8)), cfg, oz.make_plan(cfg, 8, 2, 2))
-    assert oz.kernel_launches() - before >= 4
+    assert oz.kernel_launches() - before >= 3  # slicing, pair GEMM, combine
 
 
 GEMM_VARIANTS = {
@@ -246,6 +246,9 @@ GEMM_VARIANTS = {
     "plain_1cta_bins": {"OZGPU_CTA_PAIR": "0", "OZGPU_MC": "0", "OZGPU_BINS": "1"},
     "horner_combine": {"OZGPU_COMBINE": "horner"},
     "plane_budget_row_blocks": {"OZGPU_PLANE_BUDGET_GB": "0.002"},
+    "slice_queue": {"OZGPU_SLICE_QUEUE": "1"},
+    "slice_queue_small_panels": {"OZGPU_SLICE_QUEUE": "1", "OZGPU_SLICE_PANEL_MB": "1",
+                                 "OZGPU_SLICE_LOOKAHEAD": "2"},
 }
 
 

@@ -19,24 +19,28 @@ import paper_2506_11277_b200 as oz  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=8192)
+    ap.add_argument("--m", type=int, default=0, help="rows of A (default n)")
+    ap.add_argument("--k", type=int, default=0, help="inner dimension (default n)")
     ap.add_argument("--s", type=int, nargs=2, default=[12, 12])
     ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("variants", nargs="*", default=[""])
     a = ap.parse_args()
     n = a.n
-    A = torch.from_numpy(oz.random_uniform(n, n, 1, -0.5, 0.5)).cuda()
-    B = torch.from_numpy(oz.random_uniform(n, n, 2, -0.5, 0.5)).cuda()
-    C = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    m = a.m or n
+    k = a.k or n
+    A = torch.from_numpy(oz.random_uniform(m, k, 1, -0.5, 0.5)).cuda()
+    B = torch.from_numpy(oz.random_uniform(k, n, 2, -0.5, 0.5)).cuda()
+    C = torch.empty((m, n), dtype=torch.float64, device="cuda")
     cfg = oz.MmaConfig.int8_int32()
-    plan = oz.make_plan(cfg, n, *a.s)
+    plan = oz.make_plan(cfg, k, *a.s)
     oz.set_stage_timing(True)
     ref = None
     res = {v: [] for v in a.variants}
     same = {v: True for v in a.variants}
 
     def call():
-        oz.multiply_device(n, n, n, A.data_ptr(), n, B.data_ptr(), n, C.data_ptr(), n, cfg, plan,
+        oz.multiply_device(m, n, k, A.data_ptr(), k, B.data_ptr(), n, C.data_ptr(), n, cfg, plan,
                            stream=torch.cuda.current_stream().cuda_stream)
 
     for _ in range(a.rounds):
