@@ -168,10 +168,32 @@ int ozgpu_block_ratios(ozgpu_ctx* ctx, int orientation, int64_t rows, int64_t co
                        const double* x, int64_t ldx, double* ratios_out, int* has_zero_block);
 /* abs_product / gemm_reference, proj/src/matrix.cpp:31-54, on the GPU:
  * out(i,j) = sum_r op(a_ir) op(b_rj) in binary64, r ascending, zero a_ir
- * skipped, op = |.| when absolute != 0 (identical rounding sequence). */
+ * skipped, op = |.| when absolute != 0 (identical rounding sequence; tiled
+ * through shared memory, one sequential sum per output). */
 int ozgpu_fp64_gemm(ozgpu_ctx* ctx, int absolute, int64_t m, int64_t k, int64_t n,
                     const double* a, int64_t lda, const double* b, int64_t ldb, double* out,
                     int64_t ldo);
+
+/* min_exact_slices, proj/src/slicing.cpp:212-249, on the GPU: the fewest
+ * slices of `width` bits that hold every row (orientation 0) / column (1)
+ * exactly (mode 0 truncate, 1 nearest). */
+int ozgpu_min_exact_slices(ozgpu_ctx* ctx, int orientation, int64_t rows, int64_t cols,
+                           const double* x, int64_t ldx, int width, int mode, int* out);
+/* exact_gemm(a, b).to_matrix(), proj/src/oracle.cpp:223-232 + 157-180, on the
+ * GPU: C = RN(AB) entrywise (the exact product rounded once), computed by the
+ * Ozaki-I scheme with error-free slice counts and the full pair schedule.
+ * Inputs as multiply() accepts them; OZGPU_DOMAIN_ERROR when their exponent
+ * range needs an exact value wider than 1024 bits. */
+int ozgpu_exact_gemm(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a,
+                     int64_t lda, const double* b, int64_t ldb, double* c, int64_t ldc);
+/* Error metrics, proj/src/oracle.cpp:253-292 (+ frobenius_norm :64-68), on
+ * the GPU against a reference matrix R = RN(exact): *max_elementwise = max
+ * |c - r| / |r| (0 when both are 0, +inf when only r is), *sum_sq = sum
+ * (c - r)^2; reference = NULL gives sum c^2.  Deterministic reduction order
+ * (not the reference's sequential one). */
+int ozgpu_error_metrics(ozgpu_ctx* ctx, int64_t m, int64_t n, const double* computed, int64_t ldc,
+                        const double* reference, int64_t ldr, double* max_elementwise,
+                        double* sum_sq);
 
 /* ---- the GEMM (multiply, proj/src/scheme.cpp:219-361) ------------------ */
 /* Host buffers: A m x k (lda), B k x n (ldb), C m x n (ldc), all row-major

@@ -138,6 +138,10 @@ def ref():
             [_DP, _DP]
         lib.ozref_exact_gemm.restype = ctypes.c_int
         lib.ozref_exact_gemm.argtypes = [_I64, _I64, _I64, _DP, _DP, _DP]
+        lib.ozref_fp64_gemm.restype = ctypes.c_int
+        lib.ozref_fp64_gemm.argtypes = [ctypes.c_int, _I64, _I64, _I64, _DP, _DP, _DP]
+        lib.ozref_error_metrics.restype = ctypes.c_int
+        lib.ozref_error_metrics.argtypes = [_I64, _I64, _I64, _DP, _DP, _DP, _DP, _DP]
         lib.ozref_exact_gemm_axpby.restype = ctypes.c_int
         lib.ozref_exact_gemm_axpby.argtypes = [_I64, _I64, _I64, ctypes.c_double, _DP, _DP,
                                                ctypes.c_double, _DP, _DP]
@@ -289,6 +293,25 @@ def ref_exact_gemm(a, b):
     out = np.zeros((a.shape[0], b.shape[1]))
     _rc(ref().ozref_exact_gemm(a.shape[0], a.shape[1], b.shape[1], _dp(a), _dp(b), _dp(out)))
     return out
+
+
+def ref_fp64_gemm(a, b, absolute=True):
+    """Reference abs_product (absolute) / gemm_reference (matrix.cpp:31-54)."""
+    a, b = _f64(a), _f64(b)
+    out = np.zeros((a.shape[0], b.shape[1]))
+    _rc(ref().ozref_fp64_gemm(int(absolute), a.shape[0], a.shape[1], b.shape[1], _dp(a), _dp(b),
+                              _dp(out)))
+    return out
+
+
+def ref_error_metrics(a, b, computed):
+    """Reference max_elementwise_error and normwise_gemm_error (alpha 1, beta
+    0) of `computed` against exact_gemm(a, b) (oracle.cpp:263-292)."""
+    a, b, computed = _f64(a), _f64(b), _f64(computed)
+    mx, nw = ctypes.c_double(), ctypes.c_double()
+    _rc(ref().ozref_error_metrics(a.shape[0], a.shape[1], b.shape[1], _dp(a), _dp(b),
+                                  _dp(computed), ctypes.byref(mx), ctypes.byref(nw)))
+    return mx.value, nw.value
 
 
 def ref_multiply_axpby(alpha, a, b, beta, c, sa, sb, schedule=1, strategy=2, mode=0,

@@ -313,6 +313,30 @@ int ozref_exact_gemm(std::int64_t m, std::int64_t k, std::int64_t n, const doubl
   });
 }
 
+// proj/src/matrix.cpp:31-54 (abs_product, gemm_reference)
+int ozref_fp64_gemm(int absolute, std::int64_t m, std::int64_t k, std::int64_t n,
+                    const double* a, const double* b, double* out) {
+  return guarded([&] {
+    Matrix ma = to_matrix(m, k, a), mb = to_matrix(k, n, b);
+    Matrix r = absolute ? abs_product(ma, mb) : gemm_reference(ma, mb);
+    std::memcpy(out, r.data(), sizeof(double) * m * n);
+  });
+}
+
+// proj/src/oracle.cpp:263-271 and 273-292: the metrics of `computed` against
+// exact_gemm(a, b) (beta = 0, c = 0 for the normwise one unless given)
+int ozref_error_metrics(std::int64_t m, std::int64_t k, std::int64_t n, const double* a,
+                        const double* b, const double* computed, double* max_elementwise,
+                        double* normwise) {
+  return guarded([&] {
+    Matrix ma = to_matrix(m, k, a), mb = to_matrix(k, n, b), mc = to_matrix(m, n, computed);
+    ExactProduct e = exact_gemm(ma, mb);
+    *max_elementwise = max_elementwise_error(mc, e);
+    Matrix zero(m, n);
+    *normwise = normwise_gemm_error(mc, e, ma, mb, zero, 1.0, 0.0);
+  });
+}
+
 // proj/src/oracle.cpp:234-251 (exact alpha*AB + beta*C, rounded once)
 int ozref_exact_gemm_axpby(std::int64_t m, std::int64_t k, std::int64_t n, double alpha,
                            const double* a, const double* b, double beta, const double* c,

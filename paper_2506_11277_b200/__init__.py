@@ -747,6 +747,84 @@ def abs_product(a, b, device: Optional[int] = None) -> np.ndarray:
     return out
 
 
+_sig("ozgpu_min_exact_slices", ctypes.c_int, _P, ctypes.c_int, _I64, _I64, _DP, _I64, ctypes.c_int,
+     ctypes.c_int, ctypes.POINTER(ctypes.c_int))
+_sig("ozgpu_exact_gemm", ctypes.c_int, _P, _I64, _I64, _I64, _DP, _I64, _DP, _I64, _DP, _I64)
+_sig("ozgpu_error_metrics", ctypes.c_int, _P, _I64, _I64, _DP, _I64, _DP, _I64,
+     ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double))
+
+
+def min_exact_slices(x, width: int, orientation: BlockOrientation,
+                     mode: SliceMode = SliceMode.TRUNCATE, device: Optional[int] = None) -> int:
+    """slicing.cpp:212-249 on the GPU."""
+    x = _f64(x)
+    out = ctypes.c_int()
+    _check(_lib.ozgpu_min_exact_slices(_ctx(device), int(orientation), x.shape[0], x.shape[1],
+                                       _dp(x), x.shape[1], width, int(mode), ctypes.byref(out)))
+    return out.value
+
+
+def exact_gemm(a, b, device: Optional[int] = None) -> np.ndarray:
+    """exact_gemm(a, b).to_matrix() (oracle.cpp:223-232) on the GPU: RN(AB)
+    entrywise, via error-free slices and the full pair schedule."""
+    a, b = _f64(a), _f64(b)
+    if a.shape[1] != b.shape[0]:
+        raise InvalidArgument("exact_gemm: shape mismatch")
+    out = np.empty((a.shape[0], b.shape[1]))
+    _check(_lib.ozgpu_exact_gemm(_ctx(device), a.shape[0], b.shape[1], a.shape[1], _dp(a),
+                                 a.shape[1], _dp(b), b.shape[1], _dp(out), b.shape[1]))
+    return out
+
+
+def _metrics(c, r, device):
+    c = _f64(c)
+    mx, ss = ctypes.c_double(), ctypes.c_double()
+    if r is not None:
+        r = _f64(r)
+        if r.shape != c.shape:
+            raise InvalidArgument("max_elementwise_error: shape mismatch")
+    _check(_lib.ozgpu_error_metrics(_ctx(device), c.shape[0], c.shape[1], _dp(c), c.shape[1],
+                                    _dp(r) if r is not None else None,
+                                    r.shape[1] if r is not None else 0, ctypes.byref(mx),
+                                    ctypes.byref(ss)))
+    return mx.value, ss.value
+
+
+def forward_error(computed: float, exact: float) -> float:
+    """oracle.cpp:253-261 with the exact value given as a double (RN(exact))."""
+    if exact == 0.0:
+        return 0.0 if computed == 0.0 else float("inf")
+    return abs(computed - exact) / abs(exact)
+
+
+def max_elementwise_error(computed, exact, device: Optional[int] = None) -> float:
+    """oracle.cpp:263-271 on the GPU, `exact` = RN(exact product) (e.g. from
+    exact_gemm): max over entries of |c - e| / |e|.  Against the reference's
+    unrounded ExactValue the per-entry error differs by at most ~1.1 u."""
+    return _metrics(computed, exact, device)[0]
+
+
+def frobenius_norm(x, device: Optional[int] = None) -> float:
+    """oracle.cpp:64-68 on the GPU (deterministic tree order)."""
+    import math
+    return math.sqrt(_metrics(x, None, device)[1])
+
+
+def normwise_gemm_error(dhat, dref, a, b, c, alpha: float, beta: float,
+                        device: Optional[int] = None) -> float:
+    """oracle.cpp:273-292 on the GPU; `dref` = RN(exact) as the reference's
+    dexact.to_matrix()."""
+    import math
+    dhat = _f64(dhat)
+    num = math.sqrt(_metrics(dhat, dref, device)[1])
+    k = float(_f64(a).shape[1])
+    denom = (abs(alpha) * math.sqrt(k + 2.0) * frobenius_norm(a, device) *
+             frobenius_norm(b, device) + 2.0 * abs(beta) * frobenius_norm(c, device))
+    if denom == 0.0:
+        raise DomainError("normwise_gemm_error: zero denominator")
+    return num / denom
+
+
 def zeta(kappa_a: float, kappa_b: float, slices_a: int, slices_b: int, width: int) -> float:
     """analysis.cpp:70-77."""
     import math

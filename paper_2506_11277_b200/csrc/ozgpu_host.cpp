@@ -1754,6 +1754,113 @@ int ozgpu_fp64_gemm(ozgpu_ctx* ctx, int absolute, int64_t m, int64_t k, int64_t 
   });
 }
 
+int ozgpu_min_exact_slices(ozgpu_ctx* ctx, int orientation, int64_t rows, int64_t cols,
+                           const double* x, int64_t ldx, int width, int mode, int* out) {
+  return guarded([&] {
+    if (!ctx || !out) throw std::invalid_argument("min_exact_slices: null argument");
+    if (width < 1) throw std::invalid_argument("min_exact_slices: width must be >= 1");
+    if (rows < 0 || cols < 0 || ldx < cols || (rows * cols > 0 && !x))
+      throw std::invalid_argument("min_exact_slices: bad matrix");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    OZ_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    acquire_workspace(ctx, st);
+    int64_t launches = 0;
+    double* dx = static_cast<double*>(ctx->in_a.get(sizeof(double) * rows * cols + 8));
+    h2d(dx, x, rows, cols, ldx, st);
+    int* bits = static_cast<int*>(ctx->status.get(sizeof(int)));
+    auto* colmax = static_cast<unsigned long long*>(ctx->colmax.get(8 * (cols + 1)));
+    OZ_CUDA(launch_exact_bits(orientation, dx, cols, rows, cols, colmax, bits, st, &launches));
+    int hb = 0;
+    OZ_CUDA(cudaMemcpyAsync(&hb, bits, sizeof(int), cudaMemcpyDeviceToHost, st));
+    OZ_CUDA(cudaStreamSynchronize(st));
+    ctx->launches += launches;
+    // slicing.cpp:236-240
+    *out = mode == 1 ? std::max(1, (hb + 1 + width - 1) / width) : std::max(1, (hb + width - 1) / width);
+  });
+}
+
+// exact_gemm(a, b).to_matrix() (oracle.cpp:223-232, 157-180) on the GPU: the
+// Ozaki-I scheme itself with slices that hold A and B exactly (the minimal
+// truncate-mode counts, found by the GPU scan above) and the full pair
+// schedule is error-free, and the levelled-exact combine rounds the exact
+// sum once: C = RN(AB) for every entry.
+int ozgpu_exact_gemm(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a,
+                     int64_t lda, const double* b, int64_t ldb, double* c, int64_t ldc) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("exact_gemm: null context");
+    check_operands("exact_gemm", m, n, k, a, lda, b, ldb, c, ldc);
+    if (m == 0 || n == 0) return;
+    if (k == 0) {
+      for (int64_t i = 0; i < m; ++i) std::fill(c + i * ldc, c + i * ldc + n, 0.0);
+      return;
+    }
+    const ozgpu_mma_config cfg{7, 31};
+    const int t = optimal_slice_width(cfg, k);
+    int sa = 0, sb = 0;
+    if (ozgpu_min_exact_slices(ctx, 0, m, k, a, lda, t, 0, &sa) != OZGPU_OK ||
+        ozgpu_min_exact_slices(ctx, 1, k, n, b, ldb, t, 0, &sb) != OZGPU_OK)
+      throw std::runtime_error(g_error);
+    const ozgpu_plan plan = make_plan(cfg, k, sa, sb, 0, 2, 0, 53);
+    const ChunkPlan cp = build_chunks(plan, cfg, k);
+    try {
+      (void)exact_words(cp.diagonals, t, cp.chunks.size());
+    } catch (const std::invalid_argument&) {
+      throw std::domain_error("exact_gemm: the exponent range of the inputs needs " +
+                              std::to_string(sa) + " x " + std::to_string(sb) +
+                              " exact slices, beyond the 1024-bit exact combine");
+    }
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    OZ_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    acquire_workspace(ctx, st);
+    double* da = static_cast<double*>(ctx->in_a.get(sizeof(double) * m * k + 8));
+    double* db = static_cast<double*>(ctx->in_b.get(sizeof(double) * k * n + 8));
+    double* dc = static_cast<double*>(ctx->io_c.get(sizeof(double) * m * n + 8));
+    h2d(da, a, m, k, lda, st);
+    h2d(db, b, k, n, ldb, st);
+    run_multiply(ctx, m, n, k, da, k, db, n, dc, n, cfg, plan, st, nullptr, false, 1.0, 0.0,
+                 nullptr, 0);
+    int hs = 0;
+    OZ_CUDA(cudaMemcpyAsync(&hs, ctx->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    OZ_CUDA(cudaStreamSynchronize(st));
+    if (hs) throw std::invalid_argument("exact_gemm: inputs must be finite with no negative zeros");
+    d2h(c, ldc, dc, m, n, st);
+    OZ_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int ozgpu_error_metrics(ozgpu_ctx* ctx, int64_t m, int64_t n, const double* computed, int64_t ldc,
+                        const double* reference, int64_t ldr, double* max_elementwise,
+                        double* sum_sq) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("error_metrics: null context");
+    if (m < 0 || n < 0 || ldc < n || (reference && ldr < n) || (m * n > 0 && !computed))
+      throw std::invalid_argument("error_metrics: bad matrix");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    OZ_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    acquire_workspace(ctx, st);
+    int64_t launches = 0;
+    double* dcm = static_cast<double*>(ctx->in_a.get(sizeof(double) * m * n + 8));
+    h2d(dcm, computed, m, n, ldc, st);
+    double* dr = nullptr;
+    if (reference) {
+      dr = static_cast<double*>(ctx->in_b.get(sizeof(double) * m * n + 8));
+      h2d(dr, reference, m, n, ldr, st);
+    }
+    const int sd = metric_scratch_doubles();
+    double* scratch = static_cast<double*>(ctx->ratios.get(sizeof(double) * sd));
+    OZ_CUDA(launch_error_metrics(dcm, n, dr, n, m, n, scratch, st, &launches));
+    double h[2] = {0.0, 0.0};
+    OZ_CUDA(cudaMemcpyAsync(h, scratch + sd - 2, sizeof h, cudaMemcpyDeviceToHost, st));
+    OZ_CUDA(cudaStreamSynchronize(st));
+    ctx->launches += launches;
+    if (max_elementwise) *max_elementwise = h[0];
+    if (sum_sq) *sum_sq = h[1];
+  });
+}
+
 int ozgpu_dgemm(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda,
                 const double* b, int64_t ldb, double* c, int64_t ldc, ozgpu_mma_config cfg,
                 const ozgpu_plan* plan, ozgpu_diag* diag) {

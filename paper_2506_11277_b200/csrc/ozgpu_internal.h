@@ -144,6 +144,16 @@ cudaError_t launch_col_profile(const double* b, int64_t ldb, int64_t k, int64_t 
 cudaError_t launch_fp64_gemm(int absolute, int64_t m, int64_t k, int64_t n, const double* a,
                              int64_t lda, const double* b, int64_t ldb, double* out, int64_t ldo,
                              cudaStream_t st, int64_t* launches);
+// min_exact_slices bits (slicing.cpp:212-249): *bits_out = deepest fraction
+// bit position holding a set bit over all rows (orientation 0) / columns (1).
+cudaError_t launch_exact_bits(int orientation, const double* x, int64_t ldx, int64_t rows,
+                              int64_t cols, unsigned long long* colmax, int* bits_out,
+                              cudaStream_t st, int64_t* launches);
+// error metrics: scratch[2P] = {max |c-r|/|r|, sum (c-r)^2} (r null: sum c^2)
+int metric_scratch_doubles();
+cudaError_t launch_error_metrics(const double* c, int64_t ldc, const double* r, int64_t ldr,
+                                 int64_t m, int64_t n, double* scratch, cudaStream_t st,
+                                 int64_t* launches);
 cudaError_t launch_pack_i8(const int64_t* x, int64_t rows, int64_t cols, int transpose,
                            int64_t kp, int8_t* out, cudaStream_t st, int64_t* launches);
 cudaError_t launch_integer_gemm_exact(const int64_t* x, const int64_t* y, const int64_t* c,

@@ -428,27 +428,72 @@ __global__ void __launch_bounds__(256) combine_sequential_kernel(const CombineAr
   if (local_max) atomicMax(p.realized_psi, local_max);
 }
 
-// abs_product / gemm_reference (matrix.cpp:31-54): one thread per output,
-// r ascending, zero a_ir skipped, separate multiply and add roundings.
-__global__ void __launch_bounds__(256) fp64_gemm_kernel(int absolute, int64_t m, int64_t k,
-                                                        int64_t n, const double* __restrict__ a,
-                                                        int64_t lda, const double* __restrict__ b,
-                                                        int64_t ldb, double* __restrict__ out,
-                                                        int64_t ldo) {
-  const int64_t total = m * n;
-  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
-       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t i = idx / n, j = idx - i * n;
-    double acc = 0.0;
-    for (int64_t r = 0; r < k; ++r) {
-      double ar = __ldg(a + i * lda + r);
-      if (absolute) ar = fabs(ar);
-      if (ar == 0.0) continue;
-      double br = __ldg(b + r * ldb + j);
-      if (absolute) br = fabs(br);
-      acc = __dadd_rn(acc, __dmul_rn(ar, br));
+// abs_product / gemm_reference (matrix.cpp:31-54): out(i,j) = sum_r op(a_ir)
+// op(b_rj) with r ascending, zero a_ir skipped, a separate multiply and add
+// rounding per term (the reference's loop, no FMA contraction).  Each output
+// keeps that exact sequence; the parallelism is across outputs: 64 x 64
+// output tiles per CTA (4 x 4 per thread) with 16-deep K slabs of A and B
+// staged in shared memory, so A and B are read from DRAM once per tile row /
+// column instead of once per output.
+template <bool ABS>
+__global__ void __launch_bounds__(256) fp64_gemm_tiled_kernel(int64_t m, int64_t k, int64_t n,
+                                                              const double* __restrict__ a,
+                                                              int64_t lda,
+                                                              const double* __restrict__ b,
+                                                              int64_t ldb, double* __restrict__ out,
+                                                              int64_t ldo) {
+  constexpr int TM = 64, TN = 64, TK = 16;
+  __shared__ __align__(16) double As[TK][TM + 2];  // As[r][i]
+  __shared__ __align__(16) double Bs[TK][TN];      // Bs[r][j]
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int64_t i0 = static_cast<int64_t>(blockIdx.y) * TM, j0 = static_cast<int64_t>(blockIdx.x) * TN;
+  double acc[4][4];
+#pragma unroll
+  for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = 0.0;
+  for (int64_t r0 = 0; r0 < k; r0 += TK) {
+#pragma unroll
+    for (int q = 0; q < (TM * TK) / 256; ++q) {
+      const int e = tid + 256 * q, ii = e / TK, rr = e % TK;
+      const int64_t gi = i0 + ii, gr = r0 + rr;
+      const double v = (gi < m && gr < k) ? __ldg(a + gi * lda + gr) : 0.0;
+      As[rr][ii] = ABS ? fabs(v) : v;
     }
-    out[i * ldo + j] = acc;
+#pragma unroll
+    for (int q = 0; q < (TK * TN) / 256; ++q) {
+      const int e = tid + 256 * q, rr = e / TN, jj = e % TN;
+      const int64_t gr = r0 + rr, gj = j0 + jj;
+      const double v = (gr < k && gj < n) ? __ldg(b + gr * ldb + gj) : 0.0;
+      Bs[rr][jj] = ABS ? fabs(v) : v;
+    }
+    __syncthreads();
+    const int kk = k - r0 < TK ? static_cast<int>(k - r0) : TK;
+    for (int rr = 0; rr < kk; ++rr) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        av[u] = As[rr][ty * 4 + u];
+        bv[u] = Bs[rr][tx * 4 + u];
+      }
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii) {
+        if (av[ii] == 0.0) continue;  // matrix.cpp:36-37
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = __dadd_rn(acc[ii][jj], __dmul_rn(av[ii], bv[jj]));
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int ii = 0; ii < 4; ++ii) {
+    const int64_t gi = i0 + ty * 4 + ii;
+    if (gi >= m) continue;
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int64_t gj = j0 + tx * 4 + jj;
+      if (gj < n) out[gi * ldo + gj] = acc[ii][jj];
+    }
   }
 }
 
@@ -456,10 +501,196 @@ cudaError_t launch_fp64_gemm(int absolute, int64_t m, int64_t k, int64_t n, cons
                              int64_t lda, const double* b, int64_t ldb, double* out, int64_t ldo,
                              cudaStream_t st, int64_t* launches) {
   if (m * n == 0) return cudaSuccess;
-  int64_t g = (m * n + 255) / 256;
-  fp64_gemm_kernel<<<static_cast<int>(g < 148 * 16 ? g : 148 * 16), 256, 0, st>>>(
-      absolute, m, k, n, a, lda, b, ldb, out, ldo);
+  if ((m + 63) / 64 > 65535) return cudaErrorInvalidValue;
+  dim3 grid(static_cast<unsigned>((n + 63) / 64), static_cast<unsigned>((m + 63) / 64));
+  if (k == 0) return cudaMemset2DAsync(out, ldo * sizeof(double), 0, n * sizeof(double), m, st);
+  if (absolute)
+    fp64_gemm_tiled_kernel<true><<<grid, 256, 0, st>>>(m, k, n, a, lda, b, ldb, out, ldo);
+  else
+    fp64_gemm_tiled_kernel<false><<<grid, 256, 0, st>>>(m, k, n, a, lda, b, ldb, out, ldo);
   ++*launches;
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------
+// min_exact_slices (slicing.cpp:212-249): the deepest fraction bit position
+// holding a set bit, lsb_pos = q + 52 - e - ctz(significand), over every
+// block (row / column) with q = ilogb(max |x|) + 1 of its block.
+// ----------------------------------------------------------------------------
+
+__device__ __forceinline__ int deepest_bit(double v, int q) {
+  const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(v)) & 0x7FFFFFFFFFFFFFFFULL;
+  if (bits == 0) return 0;
+  const uint64_t biased = bits >> 52, frac = bits & 0xFFFFFFFFFFFFFULL;
+  const uint64_t sig = biased ? (frac | 0x10000000000000ULL) : frac;
+  const int ex = biased ? static_cast<int>(biased) - 1023 : -1022;
+  return q + 52 - ex - (__ffsll(static_cast<long long>(sig)) - 1);
+}
+
+__device__ __forceinline__ int q_of_maxbits(unsigned long long mb) {
+  if (mb == 0) return 0;
+  const int be = static_cast<int>(mb >> 52);
+  if (be > 0) return be - 1023 + 1;
+  return (63 - __clzll(static_cast<long long>(mb))) - 1074 + 1;
+}
+
+// one warp per row: max, then the deepest set bit against the row's q
+__global__ void __launch_bounds__(256) exact_bits_rows_kernel(const double* __restrict__ a,
+                                                              int64_t lda, int64_t m, int64_t k,
+                                                              int* __restrict__ bits_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  int deepest = 0;
+  for (int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       row < m; row += warps) {
+    unsigned long long mx = 0;
+    for (int64_t j = lane; j < k; j += 32) {
+      const unsigned long long t = abs_bits_m(__ldg(a + row * lda + j));
+      mx = t > mx ? t : mx;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const unsigned long long t = __shfl_xor_sync(0xFFFFFFFFu, mx, o);
+      mx = t > mx ? t : mx;
+    }
+    if (mx == 0) continue;
+    const int q = q_of_maxbits(mx);
+    for (int64_t j = lane; j < k; j += 32) deepest = max(deepest, deepest_bit(__ldg(a + row * lda + j), q));
+  }
+  deepest = __reduce_max_sync(0xFFFFFFFFu, deepest);
+  if (lane == 0 && deepest > 0) atomicMax(bits_out, deepest);
+}
+
+// thread per column, the column max precomputed (colmax)
+__global__ void __launch_bounds__(256) exact_bits_cols_kernel(
+    const double* __restrict__ b, int64_t ldb, int64_t k, int64_t n,
+    const unsigned long long* __restrict__ colmax, int* __restrict__ bits_out) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int deepest = 0;
+  if (j < n && colmax[j] != 0) {
+    const int q = q_of_maxbits(colmax[j]);
+    for (int64_t r = blockIdx.y; r < k; r += gridDim.y) deepest = max(deepest, deepest_bit(__ldg(b + r * ldb + j), q));
+  }
+  deepest = __reduce_max_sync(0xFFFFFFFFu, deepest);
+  if ((threadIdx.x & 31) == 0 && deepest > 0) atomicMax(bits_out, deepest);
+}
+
+__global__ void __launch_bounds__(256) colmax_plain_kernel(const double* __restrict__ b,
+                                                           int64_t ldb, int64_t k, int64_t n,
+                                                           unsigned long long* __restrict__ colmax) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  unsigned long long mx = 0;
+  for (int64_t r = blockIdx.y; r < k; r += gridDim.y) {
+    const unsigned long long t = abs_bits_m(__ldg(b + r * ldb + j));
+    mx = t > mx ? t : mx;
+  }
+  if (mx) atomicMax(colmax + j, mx);
+}
+
+cudaError_t launch_exact_bits(int orientation, const double* x, int64_t ldx, int64_t rows,
+                              int64_t cols, unsigned long long* colmax, int* bits_out,
+                              cudaStream_t st, int64_t* launches) {
+  cudaError_t e = cudaMemsetAsync(bits_out, 0, sizeof(int), st);
+  if (e != cudaSuccess || rows == 0 || cols == 0) return e;
+  if (orientation == 0) {
+    const int64_t g = (rows + 7) / 8;
+    exact_bits_rows_kernel<<<static_cast<int>(g < 148 * 16 ? g : 148 * 16), 256, 0, st>>>(
+        x, ldx, rows, cols, bits_out);
+    ++*launches;
+  } else {
+    e = cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * cols, st);
+    if (e != cudaSuccess) return e;
+    const int64_t gy = rows < 64 ? rows : 64;
+    dim3 grid(static_cast<unsigned>((cols + 255) / 256), static_cast<unsigned>(gy));
+    colmax_plain_kernel<<<grid, 256, 0, st>>>(x, ldx, rows, cols, colmax);
+    exact_bits_cols_kernel<<<grid, 256, 0, st>>>(x, ldx, rows, cols, colmax, bits_out);
+    *launches += 2;
+  }
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------
+// Error metrics (oracle.cpp:253-292) against a reference matrix r (RN of the
+// exact product): the worst |c - r| / |r| (0 / 0 -> 0, x / 0 -> inf) and
+// sum (c - r)^2 (r = null: sum c^2, for frobenius_norm, oracle.cpp:64-68).
+// Deterministic: fixed grid, per-CTA partials summed in order by one CTA.
+// ----------------------------------------------------------------------------
+
+constexpr int kMetricCtas = 592;
+
+__global__ void __launch_bounds__(256) metric_partials_kernel(const double* __restrict__ c,
+                                                              int64_t ldc,
+                                                              const double* __restrict__ r,
+                                                              int64_t ldr, int64_t m, int64_t n,
+                                                              double* __restrict__ part_sum,
+                                                              double* __restrict__ part_max) {
+  __shared__ double ssum[8], smax[8];
+  double sum = 0.0, worst = 0.0;
+  const int64_t total = m * n;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = idx / n, j = idx - i * n;
+    const double cv = c[i * ldc + j];
+    if (r) {
+      const double rv = r[i * ldr + j];
+      const double d = __dadd_rn(cv, -rv);
+      sum = __dadd_rn(sum, __dmul_rn(d, d));
+      double fe;
+      if (rv == 0.0)
+        fe = cv == 0.0 ? 0.0 : __longlong_as_double(0x7FF0000000000000LL);
+      else
+        fe = fabs(d) / fabs(rv);
+      worst = fe > worst ? fe : worst;
+    } else {
+      sum = __dadd_rn(sum, __dmul_rn(cv, cv));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    sum = __dadd_rn(sum, __shfl_down_sync(0xFFFFFFFFu, sum, o));
+    const double w = __shfl_down_sync(0xFFFFFFFFu, worst, o);
+    worst = w > worst ? w : worst;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    ssum[threadIdx.x >> 5] = sum;
+    smax[threadIdx.x >> 5] = worst;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0, w = 0.0;
+    for (int q = 0; q < 8; ++q) {
+      s = __dadd_rn(s, ssum[q]);
+      w = smax[q] > w ? smax[q] : w;
+    }
+    part_sum[blockIdx.x] = s;
+    part_max[blockIdx.x] = w;
+  }
+}
+
+__global__ void metric_final_kernel(const double* __restrict__ part_sum,
+                                    const double* __restrict__ part_max, int parts,
+                                    double* __restrict__ out2) {
+  if (threadIdx.x != 0) return;
+  double s = 0.0, w = 0.0;
+  for (int q = 0; q < parts; ++q) {
+    s = __dadd_rn(s, part_sum[q]);
+    w = part_max[q] > w ? part_max[q] : w;
+  }
+  out2[0] = w;
+  out2[1] = s;
+}
+
+int metric_scratch_doubles() { return 2 * kMetricCtas + 2; }
+
+cudaError_t launch_error_metrics(const double* c, int64_t ldc, const double* r, int64_t ldr,
+                                 int64_t m, int64_t n, double* scratch, cudaStream_t st,
+                                 int64_t* launches) {
+  metric_partials_kernel<<<kMetricCtas, 256, 0, st>>>(c, ldc, r, ldr, m, n, scratch,
+                                                      scratch + kMetricCtas);
+  metric_final_kernel<<<1, 32, 0, st>>>(scratch, scratch + kMetricCtas, kMetricCtas,
+                                        scratch + 2 * kMetricCtas);
+  *launches += 2;
   return cudaGetLastError();
 }
 
