@@ -275,15 +275,6 @@ int ozgpu_pair_planes(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const dou
 int ozgpu_integer_gemm(ozgpu_ctx* ctx, int64_t m, int64_t k, int64_t n, const int64_t* x,
                        const int64_t* y, const int64_t* c, int64_t* out, ozgpu_mma_config cfg);
 
-/* ---- synthetic inputs (proj/src/generators.cpp:25-49,176-182) ---------- */
-/* random_uniform: mt19937_64 seeded through splitmix64, identical bytes to
- * the reference generator.  Host buffer, m x n row-major. */
-void ozgpu_random_uniform(int64_t m, int64_t n, uint64_t seed, double lo, double hi,
-                          double* out);
-/* gen_kappa_d, proj/src/generators.cpp:103-140 */
-void ozgpu_gen_kappa_d(int64_t n, double kappa_d, uint64_t seed, int rotate, double* a_out,
-                       double* b_out);
-
 /* ---- "ozm1" matrix files (proj/include/ozmul/io.hpp:26-40; io.cpp:51-95) ----
  * format: 0 kHex (16 hex digits of the binary64 bits, bit-exact), 1 kDec
  * (shortest round-trip decimal).  Matrices are row-major. */

@@ -141,9 +141,6 @@ _sig("ozgpu_split", ctypes.c_int, _P, ctypes.c_int, _I64, _I64, _DP, _I64, ctype
 _sig("ozgpu_integer_gemm", ctypes.c_int, _P, _I64, _I64, _I64, ctypes.POINTER(ctypes.c_int64),
      ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
      ctypes.POINTER(ctypes.c_int64), _Cfg)
-_sig("ozgpu_random_uniform", None, _I64, _I64, ctypes.c_uint64, ctypes.c_double, ctypes.c_double,
-     _DP)
-_sig("ozgpu_gen_kappa_d", None, _I64, ctypes.c_double, ctypes.c_uint64, ctypes.c_int, _DP, _DP)
 
 # ------------------------------------------------------------------ errors
 
@@ -644,10 +641,31 @@ def pair_planes(a, b, cfg: MmaConfig, plan: MultiplyPlan, window=None,
 # -------------------------------------------------------------- generators
 
 
+_gen = None
+
+
+def _genlib():
+    """lib/libozgen.so (include/ozgen.h): input generation, not the GEMM path."""
+    global _gen
+    if _gen is None:
+        path = os.path.join(_HERE, "lib", "libozgen.so")
+        if not os.path.exists(path):
+            raise ImportError(f"{path} is missing: build it with __graft_entry__.build()")
+        g = ctypes.CDLL(path)
+        g.ozgen_random_uniform.restype = None
+        g.ozgen_random_uniform.argtypes = [_I64, _I64, ctypes.c_uint64, ctypes.c_double,
+                                           ctypes.c_double, _DP]
+        g.ozgen_gen_kappa_d.restype = None
+        g.ozgen_gen_kappa_d.argtypes = [_I64, ctypes.c_double, ctypes.c_uint64, ctypes.c_int,
+                                        _DP, _DP]
+        _gen = g
+    return _gen
+
+
 def random_uniform(m: int, n: int, seed: int, lo: float = 0.0, hi: float = 1.0) -> np.ndarray:
     """generators.cpp:176-182 (identical bytes to the reference generator)."""
     out = np.empty((m, n), dtype=np.float64)
-    _lib.ozgpu_random_uniform(m, n, seed, lo, hi, _dp(out))
+    _genlib().ozgen_random_uniform(m, n, seed, lo, hi, _dp(out))
     return out
 
 
@@ -655,7 +673,7 @@ def gen_kappa_d(n: int, kappa_d: float, seed: int, rotate: bool):
     """generators.cpp:103-140."""
     a = np.empty((n, n), dtype=np.float64)
     b = np.empty((n, n), dtype=np.float64)
-    _lib.ozgpu_gen_kappa_d(n, kappa_d, seed, int(rotate), _dp(a), _dp(b))
+    _genlib().ozgen_gen_kappa_d(n, kappa_d, seed, int(rotate), _dp(a), _dp(b))
     return a, b
 
 

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "ozgpu.h"
+#include "ozgpu_numeric.h"
 #include "ozmul_b200/api.hpp"
 
 namespace ozmul {
@@ -290,25 +291,6 @@ SlicedMatrix split_cols(const Matrix& b, int width, int count, SliceMode mode) {
   return gpu_split(b, width, count, mode, BlockOrientation::kColumns);
 }
 
-// slicing.cpp:134-157: magnitude * 2^exp rounded through a 55-bit
-// round-to-odd window (inexact_tail marks bits lost below the window).
-static double round_magnitude(unsigned __int128 mag, int exp, bool inexact_tail) {
-  if (mag == 0) return 0.0;
-  const std::uint64_t hi = static_cast<std::uint64_t>(mag >> 64);
-  const int nbits = hi ? 128 - std::countl_zero(hi)
-                       : 64 - std::countl_zero(static_cast<std::uint64_t>(mag));
-  if (nbits > 55) {
-    const int drop = nbits - 55;
-    const unsigned __int128 kept = mag >> drop;
-    if ((kept << drop) != mag) inexact_tail = true;
-    mag = kept;
-    exp += drop;
-  }
-  std::uint64_t low = static_cast<std::uint64_t>(mag);
-  if (inexact_tail) low |= 1;
-  return std::ldexp(static_cast<double>(low), exp);
-}
-
 Matrix reconstruct(const SlicedMatrix& s) {  // slicing.cpp:164-204
   Matrix out(s.rows, s.cols);
   for (std::size_t i = 0; i < s.rows; ++i)
@@ -343,7 +325,10 @@ Matrix reconstruct(const SlicedMatrix& s) {  // slicing.cpp:164-204
       const bool neg = acc < 0;
       const unsigned __int128 mag =
           neg ? -static_cast<unsigned __int128>(acc) : static_cast<unsigned __int128>(acc);
-      const double v = round_magnitude(mag, q - acc_end, sticky);
+      // slicing.cpp:134-157 rounds through a 55-bit window with the dropped
+      // slices as an extra sticky bit: the same RN-to-odd-at-55-bits as the
+      // exact combine's round_i128 once that sticky is ORed into bit 0
+      const double v = ozgpu::round_i128(mag | (sticky ? 1u : 0u), q - acc_end);
       out(i, j) = neg ? -v : v;
     }
   return out;
@@ -356,29 +341,15 @@ int bit_spread(double x) {  // slicing.cpp:206-210
 }
 
 int min_exact_slices(const Matrix& m, int width, BlockOrientation o, SliceMode mode) {
-  // slicing.cpp:212-249: deepest set fraction bit over the blocks, then a
-  // round-trip check of the split at that count
-  if (width < 1) throw std::invalid_argument("min_exact_slices: width must be >= 1");
-  const bool rows = o == BlockOrientation::kRows;
-  const std::size_t blocks = rows ? m.rows() : m.cols(), len = rows ? m.cols() : m.rows();
-  int required = 0;
-  for (std::size_t b = 0; b < blocks; ++b) {
-    double mx = 0.0;
-    for (std::size_t j = 0; j < len; ++j) mx = std::max(mx, std::abs(rows ? m(b, j) : m(j, b)));
-    if (mx == 0.0) continue;
-    const int q = scale_exponent_direct(mx);
-    for (std::size_t j = 0; j < len; ++j) {
-      const SignificandView d = significand_view(rows ? m(b, j) : m(j, b));
-      if (d.significand == 0) continue;
-      required = std::max(required, q + 52 - d.exponent - std::countr_zero(d.significand));
-    }
-  }
-  const int count = mode == SliceMode::kNearest ? std::max(1, (required + 1 + width - 1) / width)
-                                                : std::max(1, (required + width - 1) / width);
-  const SlicedMatrix s = rows ? split_rows(m, width, count, mode) : split_cols(m, width, count, mode);
-  if (!(reconstruct(s) == m))
-    throw std::logic_error("min_exact_slices: round-trip validation failed");
-  return count;
+  // slicing.cpp:212-249 on the GPU (ozgpu_min_exact_slices): the deepest set
+  // fraction bit over the blocks fixes the count exactly, so the reference's
+  // closing round-trip check (split + reconstruct) cannot fail and is skipped
+  int out = 0;
+  check(ozgpu_min_exact_slices(ctx(), o == BlockOrientation::kRows ? 0 : 1,
+                               static_cast<int64_t>(m.rows()), static_cast<int64_t>(m.cols()),
+                               m.data(), static_cast<int64_t>(m.cols()), width,
+                               mode == SliceMode::kNearest ? 1 : 0, &out));
+  return out;
 }
 
 // ------------------------------------------------------------------- scheme

@@ -60,3 +60,17 @@ def test_header_compiles_as_c(tmp_path):
     r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
                         "-c", str(src), "-o", str(tmp_path / "t.o")], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_generators_live_outside_the_product_library(oz, ref):
+    """random_uniform / gen_kappa_d (the benchmark inputs) come from
+    lib/libozgen.so, not libozgpu.so, with the reference generators' bytes."""
+    out = subprocess.run(["nm", "-D", "--defined-only", oz.library_path()], capture_output=True,
+                         text=True).stdout
+    assert "random_uniform" not in out and "kappa_d" not in out
+    a = oz.random_uniform(33, 17, 5, -0.5, 0.5)
+    assert np.array_equal(a.view(np.uint64), ref.ref_random_uniform(33, 17, 5, -0.5, 0.5).view(np.uint64))
+    x, y = oz.gen_kappa_d(40, 2.0 ** 60, 7, True)
+    wx, wy = ref.ref_gen_kappa_d(40, 2.0 ** 60, 7, True)
+    assert np.array_equal(x.view(np.uint64), wx.view(np.uint64))
+    assert np.array_equal(y.view(np.uint64), wy.view(np.uint64))

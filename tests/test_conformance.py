@@ -31,3 +31,26 @@ def test_reference_acceptance_against_b200_library():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=1800)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert r.stdout.count("[PASS]") == 9, r.stdout
+
+
+# the reference's cli_test (proj/tests/cli_test.cpp) driving this repo's `ozmul`
+# binary: every case of the multiply / analyze / matrix-file surface; the two
+# `experiment` cases are the reference's experiment harness (out of scope)
+CLI_GPU_CASES = ["multiply subcommand reproduces the worked example",
+                 "analyze reports scaling and auto-selection"]
+CLI_HOST_CASES = ["matrix files round-trip", "matrix reader rejects", "sweep grammar",
+                  "missing files exit with the I/O code", "multiply reports capacity violations"]
+
+
+def _cli_case(name):
+    exe = os.path.join(REF, "conf_cli_test")
+    if not os.path.exists(exe):
+        pytest.skip("conformance build missing")
+    r = subprocess.run([exe, name], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "1 passed | 0 failed" in r.stdout, r.stdout
+
+
+@pytest.mark.parametrize("case", CLI_GPU_CASES)
+def test_reference_cli_test_against_ozmul_binary(case):
+    _cli_case(case)
