@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <condition_variable>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -174,7 +175,7 @@ struct ozgpu_ctx {
   cudaEvent_t fork_ev[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> pipe_events;
   // pinned staging of pageable host A / B / C (ozgpu_dgemm)
-  ozgpu::PinnedBuf stage_a, stage_b, stage_c;
+  ozgpu::PinnedBuf stage_a, stage_b, stage_c, status_host;
   // Workspace ordering across streams: every call that touches the
   // workspace first makes its stream wait on ws_done (recorded where the
   // previous call's last use of the workspace was enqueued), and records it
@@ -1074,12 +1075,38 @@ std::string plan_error(const ozgpu_plan& p) {
   return {};
 }
 
+// The caller's pageable buffers behind a staged pipeline call (the pinned
+// staging buffers are passed as a / b / c with dense leading dimensions).
+struct HostStage {
+  const double* a;
+  int64_t lda;
+  const double* b;
+  int64_t ldb;
+  double* c;
+  int64_t ldc;
+};
+
 // Host-pointer multiply / multiply_axpby.
 void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a,
                           int64_t lda, const double* b, int64_t ldb, double* c, int64_t ldc,
                           const ozgpu_mma_config& cfg, const ozgpu_plan& p, ozgpu_diag* diag,
                           bool axpby, double alpha, double beta, const double* cin,
-                          int64_t ldcin);
+                          int64_t ldcin, const HostStage* hs = nullptr);
+
+int pipe_env(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
+// Whether host_multiply_locked takes the blocked H2D / compute / D2H pipeline.
+bool pipeline_eligible(const ozgpu_mma_config& cfg, const ozgpu_plan& p, int64_t m, int64_t n,
+                       int64_t k, bool axpby) {
+  const ValidationResult v = host_validation(cfg, p, k);
+  const bool failing = k < 1 || v.capacity_error || v.precision_error || !plan_error(p).empty();
+  const int64_t bytes = 8 * (m * k + k * n + m * n);
+  return !failing && !axpby && p.strategy == 2 && m >= 2048 && n >= 1024 && bytes >= (64 << 20) &&
+         pipe_env("OZGPU_PIPE", 1) == 1;
+}
 
 bool is_pageable(const void* ptr) {
   cudaPointerAttributes at{};
@@ -1091,12 +1118,14 @@ bool is_pageable(const void* ptr) {
 }
 
 // rows x cols doubles between strided host buffers, rows split over threads
+// (one per 16 MiB up to min(cores, 16); `threads` > 0 forces the count)
 void parallel_copy(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
-                   int64_t cols) {
+                   int64_t cols, int threads = 0) {
   if (rows == 0 || cols == 0) return;
   const int64_t bytes = rows * cols * 8;
   const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
-  const int nt = static_cast<int>(std::clamp<int64_t>(bytes >> 24, 1, std::min(hw, 16)));
+  const int nt = threads > 0 ? static_cast<int>(std::clamp<int64_t>(threads, 1, std::max<int64_t>(1, rows)))
+                             : static_cast<int>(std::clamp<int64_t>(bytes >> 24, 1, std::min(hw, 16)));
   auto work = [&](int t) {
     const int64_t r0 = rows * t / nt, r1 = rows * (t + 1) / nt;
     if (ldd == cols && lds == cols) {
@@ -1142,6 +1171,15 @@ void host_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double
                          cin, ldcin);
     return;
   }
+  if (pipeline_eligible(cfg, p, m, n, k, axpby) && pipe_env("OZGPU_STAGE_OVERLAP", 1) == 1) {
+    // the pipeline stages each A block / B panel just before its H2D copy
+    // and unstages each C block as soon as it is back (and the inputs were
+    // found clean), so the host copies overlap PCIe and the GEMMs
+    const HostStage hs{a, lda, b, ldb, c, ldc};
+    host_multiply_locked(ctx, m, n, k, sa, k, sb, n, sc, n, cfg, p, diag, axpby, alpha, beta, cin,
+                         ldcin, &hs);
+    return;
+  }
   std::thread tb([&] { parallel_copy(sb, n, b, ldb, k, n); });
   parallel_copy(sa, k, a, lda, m, k);
   tb.join();
@@ -1154,7 +1192,7 @@ void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const
                           int64_t lda, const double* b, int64_t ldb, double* c, int64_t ldc,
                           const ozgpu_mma_config& cfg, const ozgpu_plan& p, ozgpu_diag* diag,
                           bool axpby, double alpha, double beta, const double* cin,
-                          int64_t ldcin) {
+                          int64_t ldcin, const HostStage* hs) {
   cudaStream_t st = ctx->stream;
   acquire_workspace(ctx, st);
   ValidationResult v = host_validation(cfg, p, k);
@@ -1170,13 +1208,9 @@ void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const
   // block is left to copy back after the final GEMM.  Every block's C goes
   // back on the D2H stream as soon as its combine is done.  Blocking is
   // exact: scales are per row of A and per column of B.
-  const int64_t bytes = 8 * (m * k + k * n + m * n);
-  auto env_int = [](const char* name, int dflt) {
-    const char* v = std::getenv(name);
-    return v ? std::atoi(v) : dflt;
-  };
-  const bool pipeline = !failing && !axpby && p.strategy == 2 && m >= 2048 && n >= 1024 &&
-                        bytes >= (64 << 20) && env_int("OZGPU_PIPE", 1) == 1;
+  auto env_int = pipe_env;
+  const bool pipeline = pipeline_eligible(cfg, p, m, n, k, axpby);
+  if (hs && !pipeline) throw std::logic_error("host_multiply: staged overlap needs the pipeline");
   if (pipeline) {
     // ~2048-row blocks of A and ~2048-column panels of B (at least 4 each),
     // measured on B200 (PCIe ~55 GB/s each way): 8192^3 4 x 4 (35.5 ms),
@@ -1223,7 +1257,7 @@ void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const
     cb = split_cols(npan, first);
     const std::vector<int64_t> cl = split_cols(nlast, 1);
     const size_t nr = rb.size() - 1, nc = cb.size() - 1;
-    const size_t nev = 1 + nr + nc + nr * std::max(nc, cl.size()) + 4;
+    const size_t nev = 2 + nr + nc + 2 * (nr * std::max(nc, cl.size()) + 4);
     while (ctx->pipe_events.size() < nev) {
       cudaEvent_t e;
       OZ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1248,18 +1282,6 @@ void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const
     OZ_CUDA(cudaStreamWaitEvent(ctx->h2d_stream, start, 0));
     mark("start", ctx->h2d_stream);
     std::vector<cudaEvent_t> a_in(nr), b_in(nc);
-    auto copy_a = [&](size_t i) {
-      h2d(da + rb[i] * k, a + rb[i] * lda, rb[i + 1] - rb[i], k, lda, ctx->h2d_stream);
-      a_in[i] = next_event();
-      OZ_CUDA(cudaEventRecord(a_in[i], ctx->h2d_stream));
-      mark("h2d A" + std::to_string(i), ctx->h2d_stream);
-    };
-    auto copy_b = [&](size_t j) {  // panel j: k x nj, dense at db + k * c0
-      h2d(db + k * cb[j], b + cb[j], k, cb[j + 1] - cb[j], ldb, ctx->h2d_stream);
-      b_in[j] = next_event();
-      OZ_CUDA(cudaEventRecord(b_in[j], ctx->h2d_stream));
-      mark("h2d B" + std::to_string(j), ctx->h2d_stream);
-    };
     // Default (OZGPU_PIPE_MODE=rect): A blocks and B panels alternate on the copy
     // stream (A0 B0 B1 A1 B2 A2 ...) and each arrival releases the rectangle
     // of C it completes (a growing square), so the tensor cores are fed
@@ -1275,13 +1297,94 @@ void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const
         if (jb < nc && jb == 1) arrivals.push_back({'B', jb++});
         if (ia < nr) arrivals.push_back({'A', ia++});
       }
-      for (auto& ar : arrivals) ar.first == 'A' ? copy_a(ar.second) : copy_b(ar.second);
     } else {
-      copy_a(0);
-      for (size_t j = 0; j < nc; ++j) copy_b(j);
-      for (size_t i = 1; i < nr; ++i) copy_a(i);
+      arrivals.push_back({'A', 0});
+      for (size_t j = 0; j < nc; ++j) arrivals.push_back({'B', j});
+      for (size_t i = 1; i < nr; ++i) arrivals.push_back({'A', i});
     }
+    // Staged call (pageable caller buffers): a host thread copies the inputs
+    // into the pinned staging buffers a / b in arrival order; each H2D copy
+    // waits only for its own block.
+    std::atomic<size_t> staged{0};
+    std::atomic<bool> stop_staging{false};
+    std::mutex stage_mu;
+    std::condition_variable stage_cv;
+    std::thread stager;
+    const int stage_threads = std::max(
+        1, pipe_env("OZGPU_STAGE_THREADS",
+                    static_cast<int>(std::min(16u, std::max(1u, std::thread::hardware_concurrency())))));
+    if (hs) {
+      stager = std::thread([&] {
+        for (size_t q = 0; q < arrivals.size() && !stop_staging.load(); ++q) {
+          const size_t x = arrivals[q].second;
+          if (arrivals[q].first == 'A')
+            parallel_copy(const_cast<double*>(a) + rb[x] * lda, lda, hs->a + rb[x] * hs->lda,
+                          hs->lda, rb[x + 1] - rb[x], k, stage_threads);
+          else
+            parallel_copy(const_cast<double*>(b) + cb[x], ldb, hs->b + cb[x], hs->ldb, k,
+                          cb[x + 1] - cb[x], stage_threads);
+          {
+            std::lock_guard<std::mutex> lk(stage_mu);
+            staged.store(q + 1);
+          }
+          stage_cv.notify_all();
+        }
+      });
+    }
+    struct StagerJoin {
+      std::thread& th;
+      std::atomic<bool>& stop;
+      ~StagerJoin() {
+        stop.store(true);
+        if (th.joinable()) th.join();
+      }
+    } stager_join{stager, stop_staging};
+    std::vector<size_t> arrival_of_a(nr), arrival_of_b(nc);
+    for (size_t q = 0; q < arrivals.size(); ++q)
+      (arrivals[q].first == 'A' ? arrival_of_a : arrival_of_b)[arrivals[q].second] = q;
+    auto wait_staged = [&](size_t q) {
+      if (!hs) return;
+      std::unique_lock<std::mutex> lk(stage_mu);
+      stage_cv.wait(lk, [&] { return staged.load() > q; });
+    };
+    auto copy_a = [&](size_t i) {
+      wait_staged(arrival_of_a[i]);
+      h2d(da + rb[i] * k, a + rb[i] * lda, rb[i + 1] - rb[i], k, lda, ctx->h2d_stream);
+      a_in[i] = next_event();
+      OZ_CUDA(cudaEventRecord(a_in[i], ctx->h2d_stream));
+      mark("h2d A" + std::to_string(i), ctx->h2d_stream);
+    };
+    auto copy_b = [&](size_t j) {  // panel j: k x nj, dense at db + k * c0
+      wait_staged(arrival_of_b[j]);
+      h2d(db + k * cb[j], b + cb[j], k, cb[j + 1] - cb[j], ldb, ctx->h2d_stream);
+      b_in[j] = next_event();
+      OZ_CUDA(cudaEventRecord(b_in[j], ctx->h2d_stream));
+      mark("h2d B" + std::to_string(j), ctx->h2d_stream);
+    };
+    // rect: each arrival's copy is enqueued right before its compute (the
+    // copy stream's order is unchanged; a staged call then never holds back
+    // the compute of blocks already staged); panels: all copies first
+    if (!rect)
+      for (auto& ar : arrivals) ar.first == 'A' ? copy_a(ar.second) : copy_b(ar.second);
     int64_t launches = 0;
+    // staged call: the input-status flag is read right after the last
+    // slicing kernel, so C blocks can be unstaged while later GEMMs run
+    // (and never reach the caller's C when the inputs are rejected)
+    size_t slices_done = 0;
+    cudaEvent_t status_ev = nullptr;
+    int* status_pinned = hs ? static_cast<int*>(ctx->status_host.get(sizeof(int))) : nullptr;
+    if (hs && !status_pinned) throw DeviceError("page-locked status word unavailable");
+    auto after_slice = [&]() {
+      if (!hs || ++slices_done != nr + nc) return;
+      OZ_CUDA(cudaMemcpyAsync(status_pinned, status, sizeof(int), cudaMemcpyDeviceToHost, st));
+      status_ev = next_event();
+      OZ_CUDA(cudaEventRecord(status_ev, st));
+    };
+    struct CBlock {
+      int64_t r0, r1, c0, c1;
+      cudaEvent_t back;
+    };
+    std::vector<CBlock> cblocks;
     const bool queue = use_slice_queue(p.mode, t, kp);
     int* qwork = queue ? queue_work(ctx, m, n, k, kp) : nullptr;
     auto slice_a = [&](size_t i) {
@@ -1296,6 +1399,7 @@ void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const
                                   p.mode, slA + rb[i] * kp, 0, qa + rb[i], status, st, &launches,
                                   m * kp));
       mark("slice A" + std::to_string(i), st);
+      after_slice();
     };
     auto block = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1) {
       Presliced pre{slA + r0 * kp, m * kp, qa + r0, slB + c0 * kp, n * kp, qb + c0, kp};
@@ -1311,6 +1415,11 @@ void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const
                                 n * sizeof(double), (c1 - c0) * sizeof(double), r1 - r0,
                                 cudaMemcpyDeviceToHost, ctx->d2h_stream));
       mark("d2h " + tag, ctx->d2h_stream);
+      if (hs) {
+        cudaEvent_t back = next_event();
+        OZ_CUDA(cudaEventRecord(back, ctx->d2h_stream));
+        cblocks.push_back({r0, r1, c0, c1, back});
+      }
     };
     auto slice_b = [&](size_t j) {
       const int64_t nj = cb[j + 1] - cb[j];
@@ -1323,12 +1432,14 @@ void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const
         OZ_CUDA(launch_slice_cols(db + k * cb[j], nj, k, nj, kp, t, p.slices_b, p.mode,
                                   slB + cb[j] * kp, 0, qb + cb[j], colmax + cb[j], status, st,
                                   &launches, n * kp));
+      after_slice();
     };
     if (rect) {
       size_t na = 0, nbp = 0;  // A blocks / B panels sliced so far
       for (size_t q = 0; q < arrivals.size(); ++q) {
         const auto& ar = arrivals[q];
         const bool last = q + 1 == arrivals.size();
+        ar.first == 'A' ? copy_a(ar.second) : copy_b(ar.second);
         if (ar.first == 'A') {
           slice_a(ar.second);
           na = ar.second + 1;
@@ -1369,8 +1480,19 @@ void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const
     }
     }
     ctx->launches += launches;
-    int hs = 0;
-    OZ_CUDA(cudaMemcpyAsync(&hs, status, sizeof(int), cudaMemcpyDeviceToHost, ctx->d2h_stream));
+    if (hs) {
+      // unstage C block by block as each lands, once the inputs are known clean
+      OZ_CUDA(cudaEventSynchronize(status_ev));
+      if (*status_pinned == 0)
+        for (const CBlock& cbk : cblocks) {
+          OZ_CUDA(cudaEventSynchronize(cbk.back));
+          parallel_copy(hs->c + cbk.r0 * hs->ldc + cbk.c0, hs->ldc, c + cbk.r0 * ldc + cbk.c0,
+                        ldc, cbk.r1 - cbk.r0, cbk.c1 - cbk.c0, stage_threads);
+        }
+    }
+    int hs_status = 0;
+    OZ_CUDA(cudaMemcpyAsync(&hs_status, status, sizeof(int), cudaMemcpyDeviceToHost,
+                            ctx->d2h_stream));
     OZ_CUDA(cudaStreamSynchronize(ctx->d2h_stream));
     OZ_CUDA(cudaStreamSynchronize(st));
     if (trace) {
@@ -1381,7 +1503,8 @@ void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const
       }
       for (auto& mk : marks) cudaEventDestroy(mk.second);
     }
-    if (hs) throw std::invalid_argument("multiply: inputs must be finite with no negative zeros");
+    if (hs_status)
+      throw std::invalid_argument("multiply: inputs must be finite with no negative zeros");
     if (diag) *diag = make_diag(p, cfg, m, n, k, 0);
     return;
   }
@@ -1422,13 +1545,13 @@ void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const
   }
   int* psi_dev = run_multiply(ctx, m, n, k, da, k, db, n, dc, n, cfg, p, st, nullptr, axpby,
                               alpha, beta, dcin, n);
-  int hs = 0, hpsi = 0;
-  OZ_CUDA(cudaMemcpyAsync(&hs, ctx->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  int dirty = 0, hpsi = 0;
+  OZ_CUDA(cudaMemcpyAsync(&dirty, ctx->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   if (psi_dev) OZ_CUDA(cudaMemcpyAsync(&hpsi, psi_dev, sizeof(int), cudaMemcpyDeviceToHost, st));
   OZ_CUDA(cudaStreamSynchronize(st));
   // the reference throws before producing output (scheme.cpp:223-225): C is
   // copied back only for clean inputs
-  if (hs) throw std::invalid_argument("multiply: inputs must be finite with no negative zeros");
+  if (dirty) throw std::invalid_argument("multiply: inputs must be finite with no negative zeros");
   d2h(c, ldc, dc, m, n, st);
   OZ_CUDA(cudaStreamSynchronize(st));
   if (diag) *diag = make_diag(p, cfg, m, n, k, hpsi);

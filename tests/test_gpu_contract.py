@@ -88,10 +88,11 @@ def test_operand_validation(oz):
     assert (c == 8.0).all()
 
 
-@pytest.mark.parametrize("shape", [(40, 30, 20), (600, 500, 400)])
+@pytest.mark.parametrize("shape", [(40, 30, 20), (600, 500, 400), (2304, 1536, 2048)])
 def test_rejected_inputs_leave_c_untouched(oz, shape):
     """Inf / NaN / -0 inputs raise invalid_argument (scheme.cpp:223-225) and
-    the caller's C keeps its contents (unstaged path)."""
+    the caller's (pageable) C keeps its contents: the unstaged path, and the
+    staged pipeline, which unstages C blocks only once the status is read."""
     m, k, n = shape
     cfg = oz.MmaConfig.int8_int32()
     plan = oz.make_plan(cfg, k, 4, 4)
