@@ -127,6 +127,7 @@ __device__ __forceinline__ void decode_unit(int unit, const GemmArgs& p, bool fu
     } else {
       tc = decode_tile(tile, p);
     }
+    if (p.dbg & 1) tc.tm = tc.tn = 0;  // experiment: every unit on tile 0 (results invalid)
   }
 }
 __device__ __forceinline__ void decode_unit(int unit, const GemmArgs& p, bool fused,
@@ -547,19 +548,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 // ----------------------------------------------------------------------------
 
 constexpr int kPairHalfBytes = 128 * kBlockK;             // 16 KB (A or B half)
-constexpr int kPairStageBytes = 2 * kPairHalfBytes;       // per CTA
-constexpr int smem_pair(int stages) { return stages * kPairStageBytes + 1024 + 256; }
+// per-CTA stage bytes for a 256 x kPN pair tile: A 128 rows + B kPN / 2 rows
+constexpr int pair_stage_bytes(int pn) { return kPairHalfBytes + (pn / 2) * kBlockK; }
+constexpr int smem_pair(int stages, int pn = 256) { return stages * pair_stage_bytes(pn) + 1024 + 256; }
 
-template <int kPairStages>
+// kPN = 256: 256 x 256 tiles, double-buffered 256-column accumulators.
+// kPN = 512: 256 x 512 tiles (two N = 256 MMAs per K step into the two
+// TMEM halves, single-buffered): 1.5x the operand bytes per stage for 2x
+// the MMAs, so each wave of CTA pairs covers twice the C area per slice
+// byte read (fewer DRAM and L2 -> SM bytes per int8 op).
+template <int kPairStages, int kPN = 256>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     gemm_i8_pair_kernel(const __grid_constant__ CUtensorMap tma,
                         const __grid_constant__ CUtensorMap tmb, const GemmArgs p) {
+  static_assert(kPN == 256 || kPN == 512, "pair tile width");
+  constexpr int kHalves = kPN / 256;                // N = 256 MMAs per K step
+  constexpr int kAcc = kPN == 256 ? 2 : 1;          // TMEM accumulators (512 columns in all)
+  constexpr int kBStage = kHalves * kPairHalfBytes;  // this CTA's B rows per stage
+  constexpr int kStage = kPairHalfBytes + kBStage;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + kPairStages * kPairHalfBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kPairStages * kPairStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kPairStages * kStage);
   uint64_t* empty = full + kPairStages;
   uint64_t* tfull = empty + kPairStages;
   uint64_t* tempty = tfull + 2;
@@ -605,7 +617,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       tail_range(unit, p, kb0, kb1);
       decode_unit(unit, p, false, tc, c0, nc);
       const int arow = tc.tm * 256 + static_cast<int>(rank) * 128;
-      const int brow = tc.tn * kBN + static_cast<int>(rank) * 128;
+      const int brow = tc.tn * kPN + static_cast<int>(rank) * 128;
       for (int c = c0; c < c0 + nc; ++c) {
       const ChunkDesc cd = p.chunks[chunk_at(p, c)];
       for (int pr = 0; pr < cd.npairs; ++pr) {
@@ -615,17 +627,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           lockstep = lockstep_point(p, step, lockstep, seen);
           mbar_wait(&empty[stage], phase ^ 1);
           if (elect_one()) {
-            if (leader) mbar_expect_tx(&full[stage], 2 * kPairStageBytes);
+            if (leader) mbar_expect_tx(&full[stage], 2 * kStage);
             const uint32_t bar = full_leader0 + 8 * stage;
             if (p.l2_hint) {
               const uint64_t pol = p.l2_hint == 1 ? l2_policy_evict_last() : l2_policy_evict_normal();
               tma_load_3d_pair_hint(sA + stage * kPairHalfBytes, &tma, bar, kb * kBlockK, arow,
                                     l - 1, pol);
-              tma_load_3d_pair_hint(sB + stage * kPairHalfBytes, &tmb, bar, kb * kBlockK, brow,
-                                    h - 1, pol);
+#pragma unroll
+              for (int hh = 0; hh < kHalves; ++hh)
+                tma_load_3d_pair_hint(sB + stage * kBStage + hh * kPairHalfBytes, &tmb, bar,
+                                      kb * kBlockK, brow + hh * 256, h - 1, pol);
             } else {
               tma_load_3d_pair(sA + stage * kPairHalfBytes, &tma, bar, kb * kBlockK, arow, l - 1);
-              tma_load_3d_pair(sB + stage * kPairHalfBytes, &tmb, bar, kb * kBlockK, brow, h - 1);
+#pragma unroll
+              for (int hh = 0; hh < kHalves; ++hh)
+                tma_load_3d_pair(sB + stage * kBStage + hh * kPairHalfBytes, &tmb, bar,
+                                 kb * kBlockK, brow + hh * 256, h - 1);
             }
           }
           __syncwarp();
@@ -652,21 +669,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       decode_unit(unit, p, false, tc, c0, nc);
       for (int c = c0; c < c0 + nc; ++c, ++it) {
       const ChunkDesc cd = p.chunks[chunk_at(p, c)];
-      const int acc = it & 1;
-      const uint32_t aphase = (it >> 1) & 1;
+      const int acc = it % kAcc;
+      const uint32_t aphase = (it / kAcc) & 1;
       mbar_wait(&tempty[acc], aphase ^ 1);
       tc_fence_after();
-      const uint32_t tmem_d = tmem_base + acc * kBN;
+      const uint32_t tmem_d = tmem_base + acc * kPN;
       const int total = cd.npairs * (kb1 - kb0);
       for (int i = 0; i < total; ++i) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (elect_one()) {
           const uint64_t ad = ad0 + static_cast<uint64_t>(stage * (kPairHalfBytes >> 4));
-          const uint64_t bd = bd0 + static_cast<uint64_t>(stage * (kPairHalfBytes >> 4));
+          const uint64_t bd = bd0 + static_cast<uint64_t>(stage * (kBStage >> 4));
 #pragma unroll
           for (int kk = 0; kk < kBlockK / 32; ++kk)
-            tc_mma_i8_pair(tmem_d, ad + 2 * kk, bd + 2 * kk, idesc, (i | kk) != 0);
+#pragma unroll
+            for (int hh = 0; hh < kHalves; ++hh)
+              tc_mma_i8_pair(tmem_d + hh * 256, ad + 2 * kk,
+                             bd + hh * (kPairHalfBytes >> 4) + 2 * kk, idesc, (i | kk) != 0);
           tc_commit_pair(&empty[stage]);
           if (i == total - 1) tc_commit_pair(&tfull[acc]);
         }
@@ -691,20 +711,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       decode_unit(unit, p, false, tc, c0, nc);
       for (int cpos = c0; cpos < c0 + nc; ++cpos, ++it) {
       const int c = chunk_at(p, cpos);
-      const int acc = it & 1;
-      const uint32_t aphase = (it >> 1) & 1;
+      const int acc = it % kAcc;
+      const uint32_t aphase = (it / kAcc) & 1;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const int row = tc.tm * 256 + static_cast<int>(rank) * 128 + q * 32 + lane;
       int32_t* dst = p.planes + static_cast<int64_t>(c) * p.plane_stride +
                      static_cast<int64_t>(row) * p.ldp;
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * kBN;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * kPN;
 #pragma unroll 1
-      for (int s0 = 0; s0 < kBN; s0 += 32) {
+      for (int s0 = 0; s0 < kPN; s0 += 32) {
         uint32_t r[32];
         tmem_ld32(taddr + s0, r);
-        const int col0 = tc.tn * kBN + s0;
-        if (row < p.m && partial) {  // exact integer partial sums: order-free
+        const int col0 = tc.tn * kPN + s0;
+        if (p.dbg & 2) {  // experiment: no plane stores (results invalid)
+          if (r[0] == 0x7fffffffu && r[31] == 0x7fffffffu) dst[col0] = 0;
+        } else if (row < p.m && partial) {  // exact integer partial sums: order-free
           for (int v = 0; v < 32; ++v)
             if (col0 + v < p.n && r[v] != 0u) atomicAdd(dst + col0 + v, static_cast<int>(r[v]));
         } else if (row < p.m) {
@@ -745,16 +767,17 @@ __host__ inline bool needs_config(unsigned long long& done_mask) {
   return true;
 }
 
-template <int S>
+template <int S, int PN = 256>
 static cudaError_t launch_pair_t(const CUtensorMap* tma, const CUtensorMap* tmb,
                                  const GemmArgs& args, int pairs, cudaStream_t st) {
   static unsigned long long configured = 0;
   if (needs_config(configured)) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_i8_pair_kernel<S>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pair(S));
+    cudaError_t e = cudaFuncSetAttribute(gemm_i8_pair_kernel<S, PN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         smem_pair(S, PN));
     if (e != cudaSuccess) return e;
   }
-  gemm_i8_pair_kernel<S><<<2 * pairs, kGemmThreads, smem_pair(S), st>>>(*tma, *tmb, args);
+  gemm_i8_pair_kernel<S, PN><<<2 * pairs, kGemmThreads, smem_pair(S, PN), st>>>(*tma, *tmb, args);
   return cudaSuccess;
 }
 
@@ -765,12 +788,19 @@ cudaError_t launch_gemm_i8_pair(const CUtensorMap* tma, const CUtensorMap* tmb,
   if (args.total_units < pairs) pairs = args.total_units;
   if (pairs < 1) return cudaSuccess;
   const char* sv = std::getenv("OZGPU_PAIR_STAGES");
-  const int stages = sv ? std::atoi(sv) : 6;
-  cudaError_t e0 = stages == 7 ? launch_pair_t<7>(tma, tmb, args, pairs, st)
-                 : stages == 6 ? launch_pair_t<6>(tma, tmb, args, pairs, st)
-                 : stages == 5 ? launch_pair_t<5>(tma, tmb, args, pairs, st)
-                 : stages == 3 ? launch_pair_t<3>(tma, tmb, args, pairs, st)
-                               : launch_pair_t<4>(tma, tmb, args, pairs, st);
+  cudaError_t e0;
+  if (args.pair_n == 512) {  // 48 KB stages: 4 (default) or 3
+    const int stages = sv ? std::atoi(sv) : 4;
+    e0 = stages == 3 ? launch_pair_t<3, 512>(tma, tmb, args, pairs, st)
+                     : launch_pair_t<4, 512>(tma, tmb, args, pairs, st);
+  } else {
+    const int stages = sv ? std::atoi(sv) : 6;
+    e0 = stages == 7 ? launch_pair_t<7>(tma, tmb, args, pairs, st)
+       : stages == 6 ? launch_pair_t<6>(tma, tmb, args, pairs, st)
+       : stages == 5 ? launch_pair_t<5>(tma, tmb, args, pairs, st)
+       : stages == 3 ? launch_pair_t<3>(tma, tmb, args, pairs, st)
+                     : launch_pair_t<4>(tma, tmb, args, pairs, st);
+  }
   if (e0 != cudaSuccess) return e0;
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) ++*launches;

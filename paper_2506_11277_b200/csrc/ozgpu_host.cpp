@@ -472,7 +472,7 @@ void setup_lockstep(ozgpu_ctx* ctx, GemmArgs& g, const ChunkPlan& cp, const std:
   OZ_CUDA(cudaMemsetAsync(g.sync, 0, sizeof(int) * 64 * 32, st));
   g.sync_clusters = clusters;
   g.sync_steps = (g.total_units / clusters) * bin_pairs * g.kblocks;
-  g.sync_g = 64;
+  g.sync_g = g.pair_n == 512 ? 32 : 64;  // k-steps per lockstep group (measured per tile width)
   g.sync_d = 1;
   if (const char* env = std::getenv("OZGPU_SYNC_G")) g.sync_g = std::max(1, std::atoi(env));
   if (const char* env = std::getenv("OZGPU_SYNC_D")) g.sync_d = std::max(1, std::atoi(env));
@@ -766,6 +766,7 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
     g.tiles_n = tiles_n;
     if (const char* env = std::getenv("OZGPU_RASTER_G")) g.group = std::atoi(env);
     if (const char* env = std::getenv("OZGPU_L2_HINT")) g.l2_hint = std::atoi(env);
+    if (const char* env = std::getenv("OZGPU_DBG")) g.dbg = std::atoi(env);
     if (const char* env = std::getenv("OZGPU_PAIR_ORDER"))
       g.pair_order = std::string(env) == "1" && tiles_m % 2 == 0;
     if (fused) {
@@ -811,11 +812,27 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
     // without lockstep; DRAM reads 46 GB, tensor pipe 93 % active at the base
     // clock.  Without lockstep the deep ring lets the CTAs of a wave drift
     // apart and DRAM reads grow 2-3.5x.
-    const int pair_tiles = static_cast<int>(((m + 255) / 256) * tiles_n);
     bool pair = m >= 256;
     if (const char* env = std::getenv("OZGPU_CTA_PAIR")) pair = std::string(env) == "1" && m >= 256;
+    // Pair tile width (OZGPU_PAIR_N = 256 / 512).  256 x 512 tiles by default:
+    // each wave of 74 CTA pairs then covers twice the C area per slice byte
+    // it reads, and at the power cap the saved DRAM / L2 traffic buys clock.
+    // Measured on B200 (tools/gemm_ab.py, interleaved, bitwise identical):
+    // 8192^3 (12,12) 29.3 -> 27.1 ms, 16384^3 (13,12) 276.8 -> 244.3 ms,
+    // 32768^3 2141 -> 1949 ms, 4096^3 (16,17) 6.04 -> 5.72 ms, 65536 x 2048^2
+    // (12,11) 14.62 -> 14.42 ms.
+    int pair_n = n > 256 ? 512 : 256;
+    if (const char* env = std::getenv("OZGPU_PAIR_N")) pair_n = std::atoi(env) == 512 ? 512 : 256;
+    const int pair_tiles_n = static_cast<int>((n + pair_n - 1) / pair_n);
+    const int pair_tiles = static_cast<int>(((m + 255) / 256) * pair_tiles_n);
     if (pair) {
+      g.pair_n = pair_n;
+      g.tiles_n = pair_tiles_n;
       g.tiles_m = static_cast<int>((m + 255) / 256);
+      // raster groups of 16 tile rows balance a wave's A and B footprint for
+      // 256 x 512 tiles on large squares; 8 on narrow / small grids (measured)
+      if (!std::getenv("OZGPU_RASTER_G") && pair_n == 512)
+        g.group = g.tiles_m >= 32 && g.tiles_n >= 16 ? 16 : 8;
       g.total_units = pair_tiles * g.nchunks;
       bool bins = static_cast<int64_t>(pair_tiles) * g.nchunks >= 2 * static_cast<int64_t>(ctx->num_sms);
       if (const char* env = std::getenv("OZGPU_BINS")) bins = std::string(env) == "1";
@@ -863,8 +880,8 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
             const int tm = first_m + in_group % gsz, tn = in_group / gsz;
             r0 = std::min(r0, tm * 256);
             r1 = std::max(r1, tm * 256 + 256);
-            q0 = std::min(q0, tn * 256);
-            q1 = std::max(q1, tn * 256 + 256);
+            q0 = std::min(q0, tn * pair_n);
+            q1 = std::max(q1, tn * pair_n + pair_n);
           }
           r1 = static_cast<int>(std::min<int64_t>(r1, m));
           q1 = static_cast<int>(std::min<int64_t>(q1, n));

@@ -46,6 +46,12 @@ struct GemmArgs {
   // partial wave's units, each cut into tail_parts k-ranges whose partial
   // sums are added into the (pre-zeroed) plane; tail_parts = 0: off
   int tail_first, tail_parts;
+  // measurement experiments only (OZGPU_DBG, results invalid): bit 0 maps
+  // every unit of the CTA-pair kernel to tile 0 (ideal operand locality),
+  // bit 1 drops its plane stores
+  int dbg;
+  // CTA-pair kernel tile width: 256 (256 x 256 tiles) or 512 (256 x 512)
+  int pair_n;
   int32_t* planes;    // [nchunks][m][ldp] int32 chunk sums
   int64_t plane_stride;
   int64_t ldp;

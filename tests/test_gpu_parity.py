@@ -239,13 +239,17 @@ GEMM_VARIANTS = {
     "pair_bins_lockstep": {"OZGPU_BINS": "1"},
     "pair_bins_lockstep_g1": {"OZGPU_BINS": "1", "OZGPU_SYNC_G": "1", "OZGPU_SYNC_D": "1"},
     "pair_no_lockstep": {"OZGPU_BINS": "1", "OZGPU_SYNC": "0"},
-    "pair_stages4": {"OZGPU_PAIR_STAGES": "4", "OZGPU_BINS": "1"},
+    "pair_stages3": {"OZGPU_PAIR_STAGES": "3", "OZGPU_BINS": "1"},
+    "pair_n256": {"OZGPU_PAIR_N": "256", "OZGPU_BINS": "1"},
+    "pair_n256_stages4": {"OZGPU_PAIR_N": "256", "OZGPU_PAIR_STAGES": "4", "OZGPU_BINS": "1"},
     "no_bins": {"OZGPU_BINS": "0"},
     "multicast_1cta": {"OZGPU_CTA_PAIR": "0"},
     "multicast_1cta_bins_lockstep": {"OZGPU_CTA_PAIR": "0", "OZGPU_BINS": "1"},
     "plain_1cta_bins": {"OZGPU_CTA_PAIR": "0", "OZGPU_MC": "0", "OZGPU_BINS": "1"},
     "horner_combine": {"OZGPU_COMBINE": "horner"},
     "plane_budget_row_blocks": {"OZGPU_PLANE_BUDGET_GB": "0.002"},
+    "pair_n512_3stages_no_lockstep": {"OZGPU_PAIR_N": "512", "OZGPU_PAIR_STAGES": "3",
+                                      "OZGPU_SYNC": "0"},
     "slice_queue": {"OZGPU_SLICE_QUEUE": "1"},
     "slice_queue_small_panels": {"OZGPU_SLICE_QUEUE": "1", "OZGPU_SLICE_PANEL_MB": "1",
                                  "OZGPU_SLICE_LOOKAHEAD": "2"},
@@ -274,8 +278,9 @@ def _variant_cases(ref):
 
 @pytest.mark.parametrize("variant", sorted(GEMM_VARIANTS))
 def test_gemm_variants_match_reference(oz, ref, variant, monkeypatch):
-    """Every GEMM variant -- the CTA-pair (cta_group::2) kernel with and
-    without wave lockstep and at 4 / 6 stages, the B-multicast and plain
+    """Every GEMM variant -- the CTA-pair (cta_group::2) kernel with 256 x 512
+    (default) and 256 x 256 tiles, with and without wave lockstep and at 3-6
+    stages, the B-multicast and plain
     1-CTA kernels, equal-length chunk bins on / off, the fused W-word and
     folded-combine epilogues, both exact combine kernels -- is bit-exact,
     incl. ragged tiles and 3-word exact values."""
