@@ -821,7 +821,10 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
     // 8192^3 (12,12) 29.3 -> 27.1 ms, 16384^3 (13,12) 276.8 -> 244.3 ms,
     // 32768^3 2141 -> 1949 ms, 4096^3 (16,17) 6.04 -> 5.72 ms, 65536 x 2048^2
     // (12,11) 14.62 -> 14.42 ms.
-    int pair_n = n > 256 ? 512 : 256;
+    // Small products keep 256-wide tiles (enough units to fill two waves of
+    // CTA pairs: at 1024^3 (4,4) 0.027 vs 0.039 ms).
+    const int64_t units512 = ((m + 255) / 256) * ((n + 511) / 512) * static_cast<int64_t>(g.nchunks);
+    int pair_n = n > 256 && units512 >= ctx->num_sms ? 512 : 256;
     if (const char* env = std::getenv("OZGPU_PAIR_N")) pair_n = std::atoi(env) == 512 ? 512 : 256;
     const int pair_tiles_n = static_cast<int>((n + pair_n - 1) / pair_n);
     const int pair_tiles = static_cast<int>(((m + 255) / 256) * pair_tiles_n);
