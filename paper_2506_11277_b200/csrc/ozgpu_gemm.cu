@@ -675,7 +675,53 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * kPN;
       const int total = cd.npairs * (kb1 - kb0);
-      for (int i = 0; i < total; ++i) {
+      int i0 = 0;
+      if constexpr (kPN == 512) {
+        // Single-buffered 512-column accumulator: the epilogue releases
+        // columns 0-255 (tempty[0]) before 256-511 (tempty[1]).  Start the
+        // chunk with the first ring's worth of k-steps on half 0 only, then
+        // add their half-1 MMAs once half 1 is drained (the stages are
+        // released by those later commits), so half 1's drain overlaps MMAs.
+        const int lead = total < kPairStages ? total : kPairStages;
+        const int stage0 = stage;
+        const uint32_t phase0 = phase;
+        for (int i = 0; i < lead; ++i) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint64_t ad = ad0 + static_cast<uint64_t>(stage * (kPairHalfBytes >> 4));
+            const uint64_t bd = bd0 + static_cast<uint64_t>(stage * (kBStage >> 4));
+#pragma unroll
+            for (int kk = 0; kk < kBlockK / 32; ++kk)
+              tc_mma_i8_pair(tmem_d, ad + 2 * kk, bd + 2 * kk, idesc, (i | kk) != 0);
+          }
+          __syncwarp();
+          if (++stage == kPairStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mbar_wait(&tempty[1], aphase ^ 1);
+        tc_fence_after();
+        int st2 = stage0;
+        (void)phase0;
+        for (int i = 0; i < lead; ++i) {
+          if (elect_one()) {
+            const uint64_t ad = ad0 + static_cast<uint64_t>(st2 * (kPairHalfBytes >> 4));
+            const uint64_t bd = bd0 + static_cast<uint64_t>(st2 * (kBStage >> 4));
+#pragma unroll
+            for (int kk = 0; kk < kBlockK / 32; ++kk)
+              tc_mma_i8_pair(tmem_d + 256, ad + 2 * kk, bd + (kPairHalfBytes >> 4) + 2 * kk,
+                             idesc, (i | kk) != 0);
+            tc_commit_pair(&empty[st2]);
+            if (i == total - 1) tc_commit_pair(&tfull[acc]);
+          }
+          __syncwarp();
+          if (++st2 == kPairStages) st2 = 0;
+        }
+        i0 = lead;
+      }
+      for (int i = i0; i < total; ++i) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (elect_one()) {
@@ -721,6 +767,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * kPN;
 #pragma unroll 1
       for (int s0 = 0; s0 < kPN; s0 += 32) {
+        if (kPN == 512 && s0 == 256) {  // columns 0-255 drained: release half 0
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(tempty_leader0);
+        }
         uint32_t r[32];
         tmem_ld32(taddr + s0, r);
         const int col0 = tc.tn * kPN + s0;
@@ -743,7 +794,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+      // kPN = 512: tempty[1] releases columns 256-511 (half 0 went above)
+      if (lane == 0) mbar_arrive_cluster((acc || kPN == 512) ? tempty_leader1 : tempty_leader0);
       }
     }
   }

@@ -44,3 +44,31 @@ def test_our_arm_line():
     assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9
     assert d["e2e"]["h2d_bytes_per_step"] == 8 * (1024 * 1024 * 2)
     assert d["e2e"]["d2h_bytes_per_step"] == 8 * 1024 * 1024
+
+
+def test_bench_geometry_and_config_records():
+    """bench.py's sharding geometry (no GPU): strong scaling (configs[4])
+    splits the 32768^2 C over the ranks' 2-D tiles, weak scaling gives every
+    rank a full block; config records are identical between the two arms'
+    code paths for the same world size."""
+    import importlib.util
+    import numpy as np
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    for world in (1, 2, 4, 8):
+        cfg = bench.CONFIGS["c5"]
+        cover = np.zeros((8, 8), dtype=int)  # 32768 / 4096 coarse cells
+        for rank in range(world):
+            blk, m, n, gm, gn = bench.geometry(cfg, world, rank)
+            assert (gm, gn) == (32768, 32768) and m * n * world == gm * gn
+            cover[blk.row0 // 4096:blk.row1 // 4096, blk.col0 // 4096:blk.col1 // 4096] += 1
+        assert (cover == 1).all()
+        blk, m, n, gm, gn = bench.geometry(bench.CONFIGS["c2"], world, world - 1)
+        pr, pc = bench.shard.grid_for(world)
+        assert (m, n, gm, gn) == (8192, 8192, 8192 * pr, 8192 * pc)
+        r1 = bench.config_record(cfg, world, m, n, gm, gn, (13, 12))
+        r2 = bench.config_record(cfg, world, m, n, gm, gn, (13, 12))
+        assert r1 == r2 and r1["chi"] == 90 and r1["grid"] == [pr, pc]
+    assert bench.chi_of(12, 12) == 78 and bench.chunk_count(12, 12, 8192, 7) == 12
+    assert bench.sample_block(8192) == 32 and bench.slice_width(16384) == 7
