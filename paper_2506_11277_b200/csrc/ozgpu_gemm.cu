@@ -682,7 +682,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         // chunk with the first ring's worth of k-steps on half 0 only, then
         // add their half-1 MMAs once half 1 is drained (the stages are
         // released by those later commits), so half 1's drain overlaps MMAs.
-        const int lead = total < kPairStages ? total : kPairStages;
+        const int lead = p.no_half_release ? 0 : (total < kPairStages ? total : kPairStages);
+        if (p.no_half_release) {
+          mbar_wait(&tempty[1], aphase ^ 1);
+          tc_fence_after();
+        }
         const int stage0 = stage;
         const uint32_t phase0 = phase;
         for (int i = 0; i < lead; ++i) {
@@ -701,8 +705,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             phase ^= 1;
           }
         }
-        mbar_wait(&tempty[1], aphase ^ 1);
-        tc_fence_after();
+        if (lead) {
+          mbar_wait(&tempty[1], aphase ^ 1);
+          tc_fence_after();
+        }
         int st2 = stage0;
         (void)phase0;
         for (int i = 0; i < lead; ++i) {
@@ -767,7 +773,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * kPN;
 #pragma unroll 1
       for (int s0 = 0; s0 < kPN; s0 += 32) {
-        if (kPN == 512 && s0 == 256) {  // columns 0-255 drained: release half 0
+        if (kPN == 512 && s0 == 256 && !p.no_half_release) {  // columns 0-255 drained: release half 0
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(tempty_leader0);
@@ -795,7 +801,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       tc_fence_before();
       __syncwarp();
       // kPN = 512: tempty[1] releases columns 256-511 (half 0 went above)
-      if (lane == 0) mbar_arrive_cluster((acc || kPN == 512) ? tempty_leader1 : tempty_leader0);
+      if (lane == 0) {
+        if (kPN == 512 && p.no_half_release) mbar_arrive_cluster(tempty_leader0);
+        mbar_arrive_cluster((acc || kPN == 512) ? tempty_leader1 : tempty_leader0);
+      }
       }
     }
   }

@@ -767,6 +767,7 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
     if (const char* env = std::getenv("OZGPU_RASTER_G")) g.group = std::atoi(env);
     if (const char* env = std::getenv("OZGPU_L2_HINT")) g.l2_hint = std::atoi(env);
     if (const char* env = std::getenv("OZGPU_DBG")) g.dbg = std::atoi(env);
+    if (const char* env = std::getenv("OZGPU_HALF_RELEASE")) g.no_half_release = std::atoi(env) == 0;
     if (const char* env = std::getenv("OZGPU_PAIR_ORDER"))
       g.pair_order = std::string(env) == "1" && tiles_m % 2 == 0;
     if (fused) {

@@ -52,6 +52,9 @@ struct GemmArgs {
   int dbg;
   // CTA-pair kernel tile width: 256 (256 x 256 tiles) or 512 (256 x 512)
   int pair_n;
+  // kPN = 512: 1 = release the accumulator only once fully drained
+  // (OZGPU_HALF_RELEASE=0, A/B of the half-by-half release)
+  int no_half_release;
   int32_t* planes;    // [nchunks][m][ldp] int32 chunk sums
   int64_t plane_stride;
   int64_t ldp;
