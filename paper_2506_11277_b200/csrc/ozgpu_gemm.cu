@@ -550,7 +550,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 constexpr int kPairHalfBytes = 128 * kBlockK;             // 16 KB (A or B half)
 // per-CTA stage bytes for a 256 x kPN pair tile: A 128 rows + B kPN / 2 rows
 constexpr int pair_stage_bytes(int pn) { return kPairHalfBytes + (pn / 2) * kBlockK; }
-constexpr int smem_pair(int stages, int pn = 256) { return stages * pair_stage_bytes(pn) + 1024 + 256; }
+// + the epilogue's TMA-store staging: 4 warps x 2 buffers x (32 x 32 int32)
+constexpr int kPairCStage = 4 * 2 * 4096;
+constexpr int smem_pair(int stages, int pn = 256) {
+  return stages * pair_stage_bytes(pn) + kPairCStage + 1024 + 256;
+}
 
 // kPN = 256: 256 x 256 tiles, double-buffered 256-column accumulators.
 // kPN = 512: 256 x 512 tiles (two N = 256 MMAs per K step into the two
@@ -560,7 +564,8 @@ constexpr int smem_pair(int stages, int pn = 256) { return stages * pair_stage_b
 template <int kPairStages, int kPN = 256>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     gemm_i8_pair_kernel(const __grid_constant__ CUtensorMap tma,
-                        const __grid_constant__ CUtensorMap tmb, const GemmArgs p) {
+                        const __grid_constant__ CUtensorMap tmb,
+                        const __grid_constant__ CUtensorMap tmc, const GemmArgs p) {
   static_assert(kPN == 256 || kPN == 512, "pair tile width");
   constexpr int kHalves = kPN / 256;                // N = 256 MMAs per K step
   constexpr int kAcc = kPN == 256 ? 2 : 1;          // TMEM accumulators (512 columns in all)
@@ -571,7 +576,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + kPairStages * kPairHalfBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kPairStages * kStage);
+  uint32_t* cstage = reinterpret_cast<uint32_t*>(smem + kPairStages * kStage);  // 1024-aligned
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kPairStages * kStage + kPairCStage);
   uint64_t* empty = full + kPairStages;
   uint64_t* tfull = empty + kPairStages;
   uint64_t* tempty = tfull + 2;
@@ -596,6 +602,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmb)) : "memory");
+    if (p.tma_store)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmc)) : "memory");
   }
   if (warp == 2) tmem_alloc_pair(tmem_holder, kTmemCols);
   tc_fence_before();
@@ -755,6 +763,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     const int q = warp & 3;
     const uint32_t tempty_leader0 = map_to_rank(&tempty[0], 0);
     const uint32_t tempty_leader1 = map_to_rank(&tempty[1], 0);
+    uint32_t* cbuf = cstage + q * 2 * 1024;  // this warp's two 32 x 32 int32 staging tiles
+    int cb = 0;
     int it = 0;
     for (int vunit = pair; vunit < p.total_units; vunit += npairs) {
       TileCoord tc;
@@ -781,7 +791,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         uint32_t r[32];
         tmem_ld32(taddr + s0, r);
         const int col0 = tc.tn * kPN + s0;
-        if (p.dbg & 2) {  // experiment: no plane stores (results invalid)
+        if (p.tma_store && !(p.dbg & 2)) {
+          // stage the warp's 32 rows x 32 columns in shared memory (128-byte
+          // swizzle: conflict-free 16-byte writes) and let TMA write whole
+          // lines -- a plain store for a full unit, an exact int32 reduce-add
+          // for a split-k tail part; TMA clips rows >= m and columns >= n
+          uint32_t* buf = cbuf + cb * 1024;
+          if (lane == 0) bulk_wait_read<1>();  // the store that used `buf` has read it
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<uint4*>(buf + lane * 32 + ((j ^ (lane & 7)) << 2)) =
+                make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            const int row0 = tc.tm * 256 + static_cast<int>(rank) * 128 + q * 32;
+            if (partial)
+              tma_reduce_add_3d(&tmc, buf, col0, row0, c);
+            else
+              tma_store_3d(&tmc, buf, col0, row0, c);
+            bulk_commit();
+          }
+          cb ^= 1;
+        } else if (p.dbg & 2) {  // experiment: no plane stores (results invalid)
           if (r[0] == 0x7fffffffu && r[31] == 0x7fffffffu) dst[col0] = 0;
         } else if (row < p.m && partial) {  // exact integer partial sums: order-free
           for (int v = 0; v < 32; ++v)
@@ -809,6 +842,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     }
   }
 
+  if (warp >= 4 && p.tma_store && lane == 0) bulk_wait<0>();  // staged plane stores done
   tc_fence_before();
   cluster_sync();
   if (warp == 2) {
@@ -830,7 +864,8 @@ __host__ inline bool needs_config(unsigned long long& done_mask) {
 
 template <int S, int PN = 256>
 static cudaError_t launch_pair_t(const CUtensorMap* tma, const CUtensorMap* tmb,
-                                 const GemmArgs& args, int pairs, cudaStream_t st) {
+                                 const CUtensorMap* tmc, const GemmArgs& args, int pairs,
+                                 cudaStream_t st) {
   static unsigned long long configured = 0;
   if (needs_config(configured)) {
     cudaError_t e = cudaFuncSetAttribute(gemm_i8_pair_kernel<S, PN>,
@@ -838,13 +873,14 @@ static cudaError_t launch_pair_t(const CUtensorMap* tma, const CUtensorMap* tmb,
                                          smem_pair(S, PN));
     if (e != cudaSuccess) return e;
   }
-  gemm_i8_pair_kernel<S, PN><<<2 * pairs, kGemmThreads, smem_pair(S, PN), st>>>(*tma, *tmb, args);
+  gemm_i8_pair_kernel<S, PN><<<2 * pairs, kGemmThreads, smem_pair(S, PN), st>>>(*tma, *tmb, *tmc,
+                                                                               args);
   return cudaSuccess;
 }
 
 cudaError_t launch_gemm_i8_pair(const CUtensorMap* tma, const CUtensorMap* tmb,
-                                const GemmArgs& args, int num_sms, cudaStream_t st,
-                                int64_t* launches) {
+                                const CUtensorMap* tmc, const GemmArgs& args, int num_sms,
+                                cudaStream_t st, int64_t* launches) {
   int pairs = num_sms / 2;
   if (args.total_units < pairs) pairs = args.total_units;
   if (pairs < 1) return cudaSuccess;
@@ -852,15 +888,14 @@ cudaError_t launch_gemm_i8_pair(const CUtensorMap* tma, const CUtensorMap* tmb,
   cudaError_t e0;
   if (args.pair_n == 512) {  // 48 KB stages: 4 (default) or 3
     const int stages = sv ? std::atoi(sv) : 4;
-    e0 = stages == 3 ? launch_pair_t<3, 512>(tma, tmb, args, pairs, st)
-                     : launch_pair_t<4, 512>(tma, tmb, args, pairs, st);
+    e0 = stages == 3 ? launch_pair_t<3, 512>(tma, tmb, tmc, args, pairs, st)
+                     : launch_pair_t<4, 512>(tma, tmb, tmc, args, pairs, st);
   } else {
     const int stages = sv ? std::atoi(sv) : 6;
-    e0 = stages == 7 ? launch_pair_t<7>(tma, tmb, args, pairs, st)
-       : stages == 6 ? launch_pair_t<6>(tma, tmb, args, pairs, st)
-       : stages == 5 ? launch_pair_t<5>(tma, tmb, args, pairs, st)
-       : stages == 3 ? launch_pair_t<3>(tma, tmb, args, pairs, st)
-                     : launch_pair_t<4>(tma, tmb, args, pairs, st);
+    e0 = stages >= 6 ? launch_pair_t<6>(tma, tmb, tmc, args, pairs, st)  // 7 no longer fits
+       : stages == 5 ? launch_pair_t<5>(tma, tmb, tmc, args, pairs, st)
+       : stages == 3 ? launch_pair_t<3>(tma, tmb, tmc, args, pairs, st)
+                     : launch_pair_t<4>(tma, tmb, tmc, args, pairs, st);
   }
   if (e0 != cudaSuccess) return e0;
   cudaError_t e = cudaGetLastError();

@@ -300,6 +300,25 @@ CUtensorMap make_slice_map(ozgpu_ctx* ctx, const void* base, int64_t kp, int64_t
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
+// 3-D int32 tensor map over the chunk planes [nchunks][m][ldp] (element
+// strides ldp and plane), box {32 columns, 32 rows, 1}, 128-byte swizzle:
+// the pair GEMM's epilogue TMA-stores 32 x 32 tiles through it; the map's
+// extent {n, m} clips the ragged edges.
+CUtensorMap make_plane_map(ozgpu_ctx* ctx, int32_t* planes, int64_t n, int64_t m, int64_t ldp,
+                           int nchunks, int64_t plane) {
+  CUtensorMap map;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(m),
+                        static_cast<cuuint64_t>(nchunks)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ldp * 4), static_cast<cuuint64_t>(plane * 4)};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = ctx->encode(&map, CU_TENSOR_MAP_DATA_TYPE_INT32, 3, planes, dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw DeviceError("cuTensorMapEncodeTiled (planes) failed: " + std::to_string(r));
+  return map;
+}
+
 // Row stride of the slice buffers: the K extent kp (a multiple of 128) plus
 // an optional pad (OZGPU_KPAD bytes, multiple of 128; the pad is zero-filled
 // by the slicing kernels and never read by the GEMM).
@@ -901,7 +920,12 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
         }
       }
       CUtensorMap tmb2 = make_slice_map(ctx, slB, kp, n, sb, 128, plane_b, ld);
-      OZ_CUDA(launch_gemm_i8_pair(&tma, &tmb2, g, ctx->num_sms, st, &launches));
+      // chunk planes as a TMA store target (OZGPU_TMA_STORE=0: plain stores)
+      CUtensorMap tmc{};
+      g.tma_store = 1;
+      if (const char* env = std::getenv("OZGPU_TMA_STORE")) g.tma_store = std::atoi(env) != 0;
+      if (g.tma_store) tmc = make_plane_map(ctx, planes, n, m, ldp, g.nchunks, plane);
+      OZ_CUDA(launch_gemm_i8_pair(&tma, &tmb2, &tmc, g, ctx->num_sms, st, &launches));
     } else {
       g.total_units = static_cast<int>(tiles * g.nchunks);
       // Opt-in (OZGPU_EPILOGUE=final): the exact combine folded into the

@@ -55,6 +55,8 @@ struct GemmArgs {
   // kPN = 512: 1 = release the accumulator only once fully drained
   // (OZGPU_HALF_RELEASE=0, A/B of the half-by-half release)
   int no_half_release;
+  // CTA-pair kernel: write the chunk planes with TMA bulk tensor stores
+  int tma_store;
   int32_t* planes;    // [nchunks][m][ldp] int32 chunk sums
   int64_t plane_stride;
   int64_t ldp;
@@ -136,9 +138,11 @@ cudaError_t launch_gemm_i8(const CUtensorMap* tma, const CUtensorMap* tmb, const
 cudaError_t launch_gemm_i8_mc(const CUtensorMap* tma, const CUtensorMap* tmb_half,
                               const GemmArgs& args, int num_sms, cudaStream_t st,
                               int64_t* launches);
+// tmc: 3-D int32 tensor map over the chunk planes {n, m, nchunks}, box
+// {32, 32, 1}, 128-byte swizzle (used when args.tma_store)
 cudaError_t launch_gemm_i8_pair(const CUtensorMap* tma, const CUtensorMap* tmb,
-                                const GemmArgs& args, int num_sms, cudaStream_t st,
-                                int64_t* launches);
+                                const CUtensorMap* tmc, const GemmArgs& args, int num_sms,
+                                cudaStream_t st, int64_t* launches);
 int gemm_smem_bytes();
 cudaError_t launch_combine_exact(const CombineArgs& args, int words, const ChunkDesc* host_chunks,
                                  cudaStream_t st, int64_t* launches);
