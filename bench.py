@@ -68,6 +68,10 @@ CONFIGS = {
     "ns": dict(name="north star: FP64 GEMM m=n=k=16384, uniform(-0.5,0.5), estimator-chosen "
                     "slices for 1e-15",
                m=16384, n=16384, k=16384, gen="uniform", slices="estimator"),
+    # test-only: the multi-rank code path at a size two ranks can share one GPU with
+    "t2": dict(name="test: FP64 GEMM m=n=k=4096, uniform(-0.5,0.5), estimator-chosen slices, "
+                    "2-D C tiles over the ranks (strong scaling)",
+               m=4096, n=4096, k=4096, gen="uniform", slices="estimator", strong=True),
 }
 
 METRIC = "effective FP64-equiv TFLOP/s (2mnk/t) and int8 tensor-pipe % of peak vs slices"
@@ -395,6 +399,9 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-traffic", action="store_true")
     ap.add_argument("--no-north-star", action="store_true")
+    # testing the N>1 path on a single GPU: every rank on cuda:0, gloo collectives
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--same-device", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     env_world = os.environ.get("WORLD_SIZE")
@@ -423,10 +430,15 @@ def main():
 
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.same_device:
+        local = 0
     torch.cuda.set_device(local)
     os.environ["OZGPU_DEVICE"] = str(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group("gloo")
     cfg = dict(CONFIGS[args.config])
     k = cfg["k"]
     blk, m, n, gm, gn = geometry(cfg, world, rank)
@@ -748,7 +760,7 @@ def main():
             line["north_star"] = {"error": repr(e)}
 
     # weak-scaling sub-record at N > 1: every rank an 8192^3 block (configs[1])
-    if world > 1 and args.config == "c5":
+    if world > 1 and args.config in ("c5", "t2"):
         try:
             wc = dict(CONFIGS["c2"])
             aw, bw, mw, nw = load_panels(wc)

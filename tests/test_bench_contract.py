@@ -72,3 +72,19 @@ def test_bench_geometry_and_config_records():
         assert r1 == r2 and r1["chi"] == 90 and r1["grid"] == [pr, pc]
     assert bench.chi_of(12, 12) == 78 and bench.chunk_count(12, 12, 8192, 7) == 12
     assert bench.sample_block(8192) == 32 and bench.slice_width(16384) == 7
+
+
+@pytest.mark.gpu
+def test_multi_rank_bench_path_on_one_gpu():
+    """The N > 1 bench path end to end (bench.py re-launches itself under
+    torch.distributed.run, panels exist only on their owner ranks and are
+    broadcast every step, max-over-ranks timing, the weak-scaling sub-record)
+    with two ranks sharing the one GPU of this run (gloo collectives; the
+    NCCL path differs only in the process-group backend)."""
+    d = _run(["--gpus", "2", "--config", "t2", "--steps", "3", "--warmup", "3", "--no-sweep",
+              "--no-cpu-baseline", "--no-traffic", "--dist-backend", "gloo", "--same-device"],
+             900)
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
+    assert d["config"]["grid"] == [2, 1] and d["config"]["m"] == 2048
+    assert "exchange" in d and d["weak_scaling"].get("value", 0) > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 8 * (2048 * 4096 + 4096 * 4096)
