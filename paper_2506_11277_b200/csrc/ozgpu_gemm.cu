@@ -561,12 +561,20 @@ constexpr int smem_pair(int stages, int pn = 256) {
 // TMEM halves, single-buffered): 1.5x the operand bytes per stage for 2x
 // the MMAs, so each wave of CTA pairs covers twice the C area per slice
 // byte read (fewer DRAM and L2 -> SM bytes per int8 op).
-template <int kPairStages, int kPN = 256>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+// kCl = 4: clusters of two CTA pairs stacked in M (a 512 x kPN super-tile)
+// sharing the B panel: each pair loads one of the two 256-row B boxes and
+// multicasts it to the same-half CTA of the other pair, so L2 -> SM operand
+// traffic per MMA drops by a third; a stage is released only when both
+// pairs' MMAs have consumed it (empty barriers count both commits).
+template <int kPairStages, int kPN = 256, int kCl = 2>
+__global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_i8_pair_kernel(const __grid_constant__ CUtensorMap tma,
                         const __grid_constant__ CUtensorMap tmb,
                         const __grid_constant__ CUtensorMap tmc, const GemmArgs p) {
   static_assert(kPN == 256 || kPN == 512, "pair tile width");
+  static_assert(kCl == 2 || (kCl == 4 && kPN == 512), "cluster shape");
+  constexpr int kPairsPerCl = kCl / 2;
+  constexpr int kRowsPerUnit = 256 * kPairsPerCl;
   constexpr int kHalves = kPN / 256;                // N = 256 MMAs per K step
   constexpr int kAcc = kPN == 256 ? 2 : 1;          // TMEM accumulators (512 columns in all)
   constexpr int kBStage = kHalves * kPairHalfBytes;  // this CTA's B rows per stage
@@ -585,15 +593,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
-  const bool leader = rank == 0;
-  const int pair = blockIdx.x >> 1;
-  const int npairs = gridDim.x >> 1;
+  const uint32_t crank = cluster_ctarank();
+  const uint32_t prk = crank >> 1;           // CTA pair within the cluster
+  const uint32_t rank = crank & 1;           // CTA within the pair
+  const uint32_t lead_rank = crank & ~1u;    // the pair leader's cluster rank
+  const bool leader = rank == 0;             // pair leader: issues the MMAs
+  const int pair = blockIdx.x / kCl;         // cluster index (work distribution)
+  const int npairs = gridDim.x / kCl;
+  constexpr uint16_t kEmptyMask = kCl == 4 ? 0xF : 0x3;
+  const uint16_t pair_mask = static_cast<uint16_t>(0x3u << (2 * prk));
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kPairStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], kPairsPerCl);  // one commit per pair of the cluster
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -613,18 +626,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs; warp-wide loop, elected issuer) ----------------
-    const uint32_t full_leader0 = map_to_rank(&full[0], 0);
+    const uint32_t full_leader0 = map_to_rank(&full[0], lead_rank);
     int stage = 0;
     uint32_t phase = 0;
     int step = 0;               // k-steps issued by this cluster
-    bool lockstep = p.sync != nullptr && leader;
+    bool lockstep = p.sync != nullptr && crank == 0;
     int seen = -1;
     for (int vunit = pair; vunit < p.total_units; vunit += npairs) {
       TileCoord tc;
       int c0, nc, kb0, kb1, unit = vunit;
       tail_range(unit, p, kb0, kb1);
       decode_unit(unit, p, false, tc, c0, nc);
-      const int arow = tc.tm * 256 + static_cast<int>(rank) * 128;
+      const int arow = tc.tm * kRowsPerUnit + static_cast<int>(prk) * 256 + static_cast<int>(rank) * 128;
       const int brow = tc.tn * kPN + static_cast<int>(rank) * 128;
       for (int c = c0; c < c0 + nc; ++c) {
       const ChunkDesc cd = p.chunks[chunk_at(p, c)];
@@ -635,7 +648,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           lockstep = lockstep_point(p, step, lockstep, seen);
           mbar_wait(&empty[stage], phase ^ 1);
           if (elect_one()) {
-            if (leader) mbar_expect_tx(&full[stage], 2 * kStage);
+            // (OZGPU_DBG bit 2, experiment: every B box is loaded twice)
+            const int breps = (p.dbg & 4) ? 2 : 1;
+            if (leader) mbar_expect_tx(&full[stage], 2 * (kPairHalfBytes + breps * kBStage));
             const uint32_t bar = full_leader0 + 8 * stage;
             if (p.l2_hint) {
               const uint64_t pol = p.l2_hint == 1 ? l2_policy_evict_last() : l2_policy_evict_normal();
@@ -645,12 +660,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
               for (int hh = 0; hh < kHalves; ++hh)
                 tma_load_3d_pair_hint(sB + stage * kBStage + hh * kPairHalfBytes, &tmb, bar,
                                       kb * kBlockK, brow + hh * 256, h - 1, pol);
+            } else if constexpr (kCl == 4) {
+              tma_load_3d_pair(sA + stage * kPairHalfBytes, &tma, bar, kb * kBlockK, arow, l - 1);
+              // this pair's B box (hh = prk) to the same-half CTA of both pairs
+              tma_load_3d_pair_mc(sB + stage * kBStage + prk * kPairHalfBytes, &tmb, bar,
+                                  kb * kBlockK, brow + static_cast<int>(prk) * 256, h - 1,
+                                  static_cast<uint16_t>((1u << rank) | (1u << (rank + 2))));
             } else {
               tma_load_3d_pair(sA + stage * kPairHalfBytes, &tma, bar, kb * kBlockK, arow, l - 1);
+              for (int rep = 0; rep < breps; ++rep)
 #pragma unroll
-              for (int hh = 0; hh < kHalves; ++hh)
-                tma_load_3d_pair(sB + stage * kBStage + hh * kPairHalfBytes, &tmb, bar,
-                                 kb * kBlockK, brow + hh * 256, h - 1);
+                for (int hh = 0; hh < kHalves; ++hh)
+                  tma_load_3d_pair(sB + stage * kBStage + hh * kPairHalfBytes, &tmb, bar,
+                                   kb * kBlockK, brow + hh * 256, h - 1);
             }
           }
           __syncwarp();
@@ -727,8 +749,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             for (int kk = 0; kk < kBlockK / 32; ++kk)
               tc_mma_i8_pair(tmem_d + 256, ad + 2 * kk, bd + (kPairHalfBytes >> 4) + 2 * kk,
                              idesc, (i | kk) != 0);
-            tc_commit_pair(&empty[st2]);
-            if (i == total - 1) tc_commit_pair(&tfull[acc]);
+            tc_commit_pair_mask(&empty[st2], kEmptyMask);
+            if (i == total - 1) tc_commit_pair_mask(&tfull[acc], pair_mask);
           }
           __syncwarp();
           if (++st2 == kPairStages) st2 = 0;
@@ -747,8 +769,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             for (int hh = 0; hh < kHalves; ++hh)
               tc_mma_i8_pair(tmem_d + hh * 256, ad + 2 * kk,
                              bd + hh * (kPairHalfBytes >> 4) + 2 * kk, idesc, (i | kk) != 0);
-          tc_commit_pair(&empty[stage]);
-          if (i == total - 1) tc_commit_pair(&tfull[acc]);
+          tc_commit_pair_mask(&empty[stage], kEmptyMask);
+          if (i == total - 1) tc_commit_pair_mask(&tfull[acc], pair_mask);
         }
         __syncwarp();
         if (++stage == kPairStages) {
@@ -761,8 +783,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   } else if (warp >= 4) {
     // ---------------- epilogue (both CTAs): TMEM -> int32 chunk plane ----------------
     const int q = warp & 3;
-    const uint32_t tempty_leader0 = map_to_rank(&tempty[0], 0);
-    const uint32_t tempty_leader1 = map_to_rank(&tempty[1], 0);
+    const uint32_t tempty_leader0 = map_to_rank(&tempty[0], lead_rank);
+    const uint32_t tempty_leader1 = map_to_rank(&tempty[1], lead_rank);
     uint32_t* cbuf = cstage + q * 2 * 1024;  // this warp's two 32 x 32 int32 staging tiles
     int cb = 0;
     int it = 0;
@@ -777,7 +799,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const uint32_t aphase = (it / kAcc) & 1;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
-      const int row = tc.tm * 256 + static_cast<int>(rank) * 128 + q * 32 + lane;
+      const int row = tc.tm * kRowsPerUnit + static_cast<int>(prk) * 256 +
+                      static_cast<int>(rank) * 128 + q * 32 + lane;
       int32_t* dst = p.planes + static_cast<int64_t>(c) * p.plane_stride +
                      static_cast<int64_t>(row) * p.ldp;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * kPN;
@@ -806,7 +829,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            const int row0 = tc.tm * 256 + static_cast<int>(rank) * 128 + q * 32;
+            const int row0 = tc.tm * kRowsPerUnit + static_cast<int>(prk) * 256 +
+                             static_cast<int>(rank) * 128 + q * 32;
             if (partial)
               tma_reduce_add_3d(&tmc, buf, col0, row0, c);
             else
@@ -862,31 +886,46 @@ __host__ inline bool needs_config(unsigned long long& done_mask) {
   return true;
 }
 
-template <int S, int PN = 256>
+template <int S, int PN = 256, int CL = 2>
 static cudaError_t launch_pair_t(const CUtensorMap* tma, const CUtensorMap* tmb,
-                                 const CUtensorMap* tmc, const GemmArgs& args, int pairs,
+                                 const CUtensorMap* tmc, const GemmArgs& args, int clusters,
                                  cudaStream_t st) {
   static unsigned long long configured = 0;
   if (needs_config(configured)) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_i8_pair_kernel<S, PN>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_i8_pair_kernel<S, PN, CL>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          smem_pair(S, PN));
     if (e != cudaSuccess) return e;
   }
-  gemm_i8_pair_kernel<S, PN><<<2 * pairs, kGemmThreads, smem_pair(S, PN), st>>>(*tma, *tmb, *tmc,
-                                                                               args);
-  return cudaSuccess;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(CL * clusters);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = smem_pair(S, PN);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemm_i8_pair_kernel<S, PN, CL>, *tma, *tmb, *tmc, args);
 }
 
 cudaError_t launch_gemm_i8_pair(const CUtensorMap* tma, const CUtensorMap* tmb,
                                 const CUtensorMap* tmc, const GemmArgs& args, int num_sms,
                                 cudaStream_t st, int64_t* launches) {
-  int pairs = num_sms / 2;
+  const int cl = args.cluster_ctas == 4 ? 4 : 2;
+  int pairs = args.max_clusters > 0 ? args.max_clusters : num_sms / cl;  // clusters
   if (args.total_units < pairs) pairs = args.total_units;
   if (pairs < 1) return cudaSuccess;
   const char* sv = std::getenv("OZGPU_PAIR_STAGES");
   cudaError_t e0;
-  if (args.pair_n == 512) {  // 48 KB stages: 4 (default) or 3
+  if (args.pair_n == 512 && cl == 4) {
+    const int stages = sv ? std::atoi(sv) : 4;
+    e0 = stages == 3 ? launch_pair_t<3, 512, 4>(tma, tmb, tmc, args, pairs, st)
+                     : launch_pair_t<4, 512, 4>(tma, tmb, tmc, args, pairs, st);
+  } else if (args.pair_n == 512) {  // 48 KB stages: 4 (default) or 3
     const int stages = sv ? std::atoi(sv) : 4;
     e0 = stages == 3 ? launch_pair_t<3, 512>(tma, tmb, tmc, args, pairs, st)
                      : launch_pair_t<4, 512>(tma, tmb, tmc, args, pairs, st);

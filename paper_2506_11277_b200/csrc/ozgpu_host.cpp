@@ -475,19 +475,27 @@ bool build_bins(const std::vector<ChunkDesc>& chunks, std::vector<int>& order,
   return false;
 }
 
+// Co-resident clusters of the CTA-pair kernel: 4-CTA clusters cannot tile
+// every GPC of the 148-SM part (33 fit, OZGPU_QUAD_CLUSTERS overrides).
+int max_pair_clusters(int num_sms, int cluster_ctas) {
+  if (cluster_ctas != 4) return num_sms / 2;
+  if (const char* env = std::getenv("OZGPU_QUAD_CLUSTERS")) return std::max(1, std::atoi(env));
+  return num_sms * 33 / 148;
+}
+
 // Wave lockstep of the 2-CTA GEMM kernels (GemmArgs::sync): equal-length
 // units (bins) only; OZGPU_SYNC=0/1, OZGPU_SYNC_G / OZGPU_SYNC_D override the
 // group size and the allowed lag in groups.
 void setup_lockstep(ozgpu_ctx* ctx, GemmArgs& g, const ChunkPlan& cp, const std::vector<int>& aux,
-                    const std::vector<int>& bfirst, cudaStream_t st) {
+                    const std::vector<int>& bfirst, cudaStream_t st, DevBuf& sync_buf) {
   if (!g.bin_first || bfirst.size() < 2) return;
   bool sync = true;
   if (const char* env = std::getenv("OZGPU_SYNC")) sync = std::string(env) == "1";
   if (!sync) return;
-  const int clusters = std::min(ctx->num_sms / 2, g.total_units);
+  const int clusters = std::min(max_pair_clusters(ctx->num_sms, g.cluster_ctas), g.total_units);
   int bin_pairs = 0;
   for (int q = bfirst[0]; q < bfirst[1]; ++q) bin_pairs += cp.chunks[aux[q]].npairs;
-  g.sync = static_cast<int*>(ctx->sync.get(sizeof(int) * 64 * 32));
+  g.sync = static_cast<int*>(sync_buf.get(sizeof(int) * 64 * 32));
   OZ_CUDA(cudaMemsetAsync(g.sync, 0, sizeof(int) * 64 * 32, st));
   g.sync_clusters = clusters;
   g.sync_steps = (g.total_units / clusters) * bin_pairs * g.kblocks;
@@ -846,33 +854,46 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
     const int64_t units512 = ((m + 255) / 256) * ((n + 511) / 512) * static_cast<int64_t>(g.nchunks);
     int pair_n = n > 256 && units512 >= ctx->num_sms ? 512 : 256;
     if (const char* env = std::getenv("OZGPU_PAIR_N")) pair_n = std::atoi(env) == 512 ? 512 : 256;
-    const int pair_tiles_n = static_cast<int>((n + pair_n - 1) / pair_n);
-    const int pair_tiles = static_cast<int>(((m + 255) / 256) * pair_tiles_n);
-    if (pair) {
-      g.pair_n = pair_n;
-      g.tiles_n = pair_tiles_n;
-      g.tiles_m = static_cast<int>((m + 255) / 256);
+    // One launch of the CTA-pair kernel over C rows [row0, row0 + rows) with
+    // clusters of `cl` CTAs (2: one pair; 4: two pairs stacked in M sharing
+    // the B panel by multicast, 512-wide tiles only), its own lockstep
+    // counters and split-k tail.
+    bool bins_ok = false;  // set below, before the launches
+    std::vector<int> bfirst;
+    int* daux = nullptr;
+    auto launch_pair_part = [&](int64_t row0, int64_t rows, int cl, cudaStream_t pst,
+                                DevBuf& sync_buf) {
+      GemmArgs gp = g;
+      const int unit_rows = 128 * cl;  // 256 per CTA pair
+      const int pair_tiles_n = static_cast<int>((n + pair_n - 1) / pair_n);
+      const int pair_tiles =
+          static_cast<int>(((rows + unit_rows - 1) / unit_rows) * pair_tiles_n);
+      gp.m = static_cast<int>(rows);
+      gp.pair_n = pair_n;
+      gp.cluster_ctas = cl;
+      gp.max_clusters = max_pair_clusters(ctx->num_sms, cl);
+      gp.tiles_n = pair_tiles_n;
+      gp.tiles_m = static_cast<int>((rows + unit_rows - 1) / unit_rows);
       // raster groups of 16 tile rows balance a wave's A and B footprint for
       // 256 x 512 tiles on large squares; 8 on narrow / small grids (measured)
       if (!std::getenv("OZGPU_RASTER_G") && pair_n == 512)
-        g.group = g.tiles_m >= 32 && g.tiles_n >= 16 ? 16 : 8;
-      g.total_units = pair_tiles * g.nchunks;
-      bool bins = static_cast<int64_t>(pair_tiles) * g.nchunks >= 2 * static_cast<int64_t>(ctx->num_sms);
+        gp.group = cl == 4 ? (gp.tiles_m >= 16 && gp.tiles_n >= 16 ? 8 : 4)
+                           : (gp.tiles_m >= 32 && gp.tiles_n >= 16 ? 16 : 8);
+      gp.total_units = pair_tiles * gp.nchunks;
+      bool bins = static_cast<int64_t>(pair_tiles) * gp.nchunks >= 2 * static_cast<int64_t>(ctx->num_sms);
       if (const char* env = std::getenv("OZGPU_BINS")) bins = std::string(env) == "1";
       std::vector<int>& aux = ctx->host_aux;
-      std::vector<int> bfirst;
-      if (bins && build_bins(cp.chunks, aux, bfirst)) {
+      std::vector<int> no_bins;
+      const std::vector<int>& bf = bins && bins_ok ? bfirst : no_bins;
+      if (bins && bins_ok) {
         const size_t nb = bfirst.size() - 1;
-        aux.insert(aux.end(), bfirst.begin(), bfirst.end());
-        int* daux = static_cast<int*>(ctx->aux.get(sizeof(int) * aux.size()));
-        upload_table(ctx, daux, aux.data(), sizeof(int) * aux.size(), st);
-        g.proc_order = daux;
-        g.bin_first = daux + g.nchunks;
-        g.total_units = static_cast<int>(static_cast<int64_t>(pair_tiles) * nb);
+        gp.proc_order = daux;
+        gp.bin_first = daux + gp.nchunks;
+        gp.total_units = static_cast<int>(static_cast<int64_t>(pair_tiles) * nb);
       }
-      setup_lockstep(ctx, g, cp, aux, bfirst, st);
+      setup_lockstep(ctx, gp, cp, aux, bf, pst, sync_buf);
       // Split-k tail (OZGPU_TAIL_SPLIT=0 turns it off): the R units of the
-      // last partial wave (equal-length units on C CTA pairs, R = U mod C) are
+      // last partial wave (equal-length units on C clusters, R = U mod C) are
       // each cut into P = C / R k-ranges that run side by side and add their
       // exact int32 partial sums into the plane (zeroed here over the tail
       // tiles' bounding box; the other tiles in the box are stored later in
@@ -881,51 +902,75 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
       {
         bool tail = true;
         if (const char* env = std::getenv("OZGPU_TAIL_SPLIT")) tail = std::string(env) == "1";
-        const int clusters = std::min(ctx->num_sms / 2, g.total_units);
-        const int U = g.total_units;
+        const int clusters = std::min(max_pair_clusters(ctx->num_sms, cl), gp.total_units);
+        const int U = gp.total_units;
         const int R = clusters > 0 ? U % clusters : 0;
         // at most 512 (part, chunk) plane tiles of atomic adds (32 M int32
         // adds): bins of many short chunks (k = 32768) get fewer parts
-        const int nc_last = bfirst.size() >= 2
-                                ? bfirst[bfirst.size() - 1] - bfirst[bfirst.size() - 2]
-                                : 1;
+        const int nc_last = bf.size() >= 2 ? bf[bf.size() - 1] - bf[bf.size() - 2] : 1;
         const int P = R ? std::min(clusters / R, 512 / (R * std::max(1, nc_last))) : 0;
-        if (tail && g.bin_first && R && P >= 2 && pair_tiles >= R && g.kblocks >= P &&
+        if (tail && gp.bin_first && R && P >= 2 && pair_tiles >= R && gp.kblocks >= P &&
             U >= clusters) {
-          const int G = g.group > 0 ? g.group : 8;
+          const int G = gp.group > 0 ? gp.group : 8;
           int r0 = INT32_MAX, r1 = 0, q0 = INT32_MAX, q1 = 0;
           for (int u = U - R; u < U; ++u) {
             const int tile = u % pair_tiles;  // the last bin (R <= pair_tiles)
-            const int group_size = G * g.tiles_n;
+            const int group_size = G * gp.tiles_n;
             const int grp = tile / group_size, first_m = grp * G;
-            const int gsz = std::min(G, g.tiles_m - first_m);
+            const int gsz = std::min(G, gp.tiles_m - first_m);
             const int in_group = tile - grp * group_size;
             const int tm = first_m + in_group % gsz, tn = in_group / gsz;
-            r0 = std::min(r0, tm * 256);
-            r1 = std::max(r1, tm * 256 + 256);
+            r0 = std::min(r0, tm * unit_rows);
+            r1 = std::max(r1, tm * unit_rows + unit_rows);
             q0 = std::min(q0, tn * pair_n);
             q1 = std::max(q1, tn * pair_n + pair_n);
           }
-          r1 = static_cast<int>(std::min<int64_t>(r1, m));
+          r1 = static_cast<int>(std::min<int64_t>(r1, rows));
           q1 = static_cast<int>(std::min<int64_t>(q1, n));
-          const size_t nb = bfirst.size() - 1;
-          for (int q = bfirst[nb - 1]; q < bfirst[nb]; ++q)
+          const size_t nb = bf.size() - 1;
+          for (int q = bf[nb - 1]; q < bf[nb]; ++q)
             OZ_CUDA(cudaMemset2DAsync(planes + static_cast<int64_t>(aux[q]) * plane +
-                                          static_cast<int64_t>(r0) * ldp + q0,
+                                          (row0 + static_cast<int64_t>(r0)) * ldp + q0,
                                       sizeof(int32_t) * ldp, 0, sizeof(int32_t) * (q1 - q0),
-                                      r1 - r0, st));
-          g.tail_first = U - R;
-          g.tail_parts = P;
-          g.total_units = U - R + R * P;
+                                      r1 - r0, pst));
+          gp.tail_first = U - R;
+          gp.tail_parts = P;
+          gp.total_units = U - R + R * P;
         }
       }
+      CUtensorMap tma_p = make_slice_map(ctx, slA + row0 * ld, kp, rows, sa, kBlockM, plane_a, ld);
       CUtensorMap tmb2 = make_slice_map(ctx, slB, kp, n, sb, 128, plane_b, ld);
       // chunk planes as a TMA store target (OZGPU_TMA_STORE=0: plain stores)
       CUtensorMap tmc{};
-      g.tma_store = 1;
-      if (const char* env = std::getenv("OZGPU_TMA_STORE")) g.tma_store = std::atoi(env) != 0;
-      if (g.tma_store) tmc = make_plane_map(ctx, planes, n, m, ldp, g.nchunks, plane);
-      OZ_CUDA(launch_gemm_i8_pair(&tma, &tmb2, &tmc, g, ctx->num_sms, st, &launches));
+      gp.tma_store = 1;
+      if (const char* env = std::getenv("OZGPU_TMA_STORE")) gp.tma_store = std::atoi(env) != 0;
+      gp.planes = planes + row0 * ldp;
+      if (gp.tma_store) tmc = make_plane_map(ctx, gp.planes, n, rows, ldp, gp.nchunks, plane);
+      OZ_CUDA(launch_gemm_i8_pair(&tma_p, &tmb2, &tmc, gp, ctx->num_sms, pst, &launches));
+    };
+    if (pair) {
+      // the bin table (built and uploaded once)
+      bins_ok = build_bins(cp.chunks, ctx->host_aux, bfirst);
+      if (bins_ok) {
+        std::vector<int>& aux = ctx->host_aux;
+        aux.insert(aux.end(), bfirst.begin(), bfirst.end());
+        daux = static_cast<int*>(ctx->aux.get(sizeof(int) * aux.size()));
+        upload_table(ctx, daux, aux.data(), sizeof(int) * aux.size(), st);
+      }
+      // OZGPU_QUAD=1 (opt-in): 4-CTA clusters, two CTA pairs stacked in M
+      // sharing the B panel by multicast.  Measured on B200 at 8192^3 (12,12):
+      // the multicast saves energy (SM clock 1436 -> 1507 MHz at the cap) but
+      // only 33 such clusters fit on the 148 SMs (132 used): 28.6 vs 27.1 ms.
+      // Running the last rows concurrently on 2-CTA clusters over the 16 idle
+      // SMs was bitwise exact but 46 ms -- the hardware places the second
+      // kernel's clusters on SMs the first one needs, stalling its lockstep.
+      int quad = 0;
+      if (const char* env = std::getenv("OZGPU_QUAD")) quad = std::atoi(env);
+      if (quad == 1 && pair_n == 512 && m >= 512) {
+        launch_pair_part(0, m, 4, st, ctx->sync);
+      } else {
+        launch_pair_part(0, m, 2, st, ctx->sync);
+      }
     } else {
       g.total_units = static_cast<int>(tiles * g.nchunks);
       // Opt-in (OZGPU_EPILOGUE=final): the exact combine folded into the
@@ -1007,7 +1052,7 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
       if (mc) {
         const int64_t super_tiles = static_cast<int64_t>((tiles_m + 1) / 2) * tiles_n;
         g.total_units = static_cast<int>(g.total_units / tiles * super_tiles);
-        setup_lockstep(ctx, g, cp, aux, bfirst, st);
+        setup_lockstep(ctx, g, cp, aux, bfirst, st, ctx->sync);
         CUtensorMap tmb_half = make_slice_map(ctx, slB, kp, n, sb, 128, plane_b, ld);
         OZ_CUDA(launch_gemm_i8_mc(&tma, &tmb_half, g, ctx->num_sms, st, &launches));
       } else {

@@ -48,7 +48,7 @@ struct GemmArgs {
   int tail_first, tail_parts;
   // measurement experiments only (OZGPU_DBG, results invalid): bit 0 maps
   // every unit of the CTA-pair kernel to tile 0 (ideal operand locality),
-  // bit 1 drops its plane stores
+  // bit 1 drops its plane stores, bit 2 loads every B box twice (+L2 traffic)
   int dbg;
   // CTA-pair kernel tile width: 256 (256 x 256 tiles) or 512 (256 x 512)
   int pair_n;
@@ -57,6 +57,10 @@ struct GemmArgs {
   int no_half_release;
   // CTA-pair kernel: write the chunk planes with TMA bulk tensor stores
   int tma_store;
+  // CTA-pair kernel cluster size: 2 (one pair) or 4 (two pairs stacked in M
+  // sharing the B panel by multicast; pair_n 512 only)
+  int cluster_ctas;
+  int max_clusters;  // co-resident clusters to launch (0 = num_sms / cluster_ctas)
   int32_t* planes;    // [nchunks][m][ldp] int32 chunk sums
   int64_t plane_stride;
   int64_t ldp;

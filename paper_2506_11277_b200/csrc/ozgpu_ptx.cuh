@@ -165,6 +165,28 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
       "h"(static_cast<uint16_t>(3))
       : "memory");
 }
+// commit the leader's MMAs to the same mbarrier offset in the CTAs of `mask`
+__device__ __forceinline__ void tc_commit_pair_mask(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_addr(bar)),
+      "h"(mask)
+      : "memory");
+}
+// CTA-pair TMA load multicast to the CTAs of `mask` (the box lands at the same
+// smem offset in each); the complete_tx bytes go to each destination pair's
+// leader barrier at the offset of bar_cluster_addr (the issuing pair's
+// leader barrier)
+__device__ __forceinline__ void tma_load_3d_pair_mc(void* dst, const CUtensorMap* map,
+                                                    uint32_t bar_cluster_addr, int c0, int c1,
+                                                    int c2, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::"
+      "bytes.multicast::cluster [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster_addr), "r"(c0), "r"(c1), "r"(c2),
+      "h"(mask)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_alloc_pair(uint32_t* holder, uint32_t cols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                    smem_addr(holder)),

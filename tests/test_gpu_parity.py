@@ -250,6 +250,7 @@ GEMM_VARIANTS = {
     "plane_budget_row_blocks": {"OZGPU_PLANE_BUDGET_GB": "0.002"},
     "pair_n512_3stages_no_lockstep": {"OZGPU_PAIR_N": "512", "OZGPU_PAIR_STAGES": "3",
                                       "OZGPU_SYNC": "0"},
+    "quad_clusters": {"OZGPU_QUAD": "1", "OZGPU_BINS": "1"},
     "slice_queue": {"OZGPU_SLICE_QUEUE": "1"},
     "slice_queue_small_panels": {"OZGPU_SLICE_QUEUE": "1", "OZGPU_SLICE_PANEL_MB": "1",
                                  "OZGPU_SLICE_LOOKAHEAD": "2"},
