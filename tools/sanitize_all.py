@@ -22,7 +22,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2506_11277_b200 as oz  # noqa: E402
 
 CASES = [
-    ("default (CTA pair, bins, lockstep, split-k tail)", {}),
+    ("default (CTA pair 256x512, bins, lockstep, split-k tail, TMA-stored planes)", {}),
+    ("CTA pair 256x256", {"OZGPU_PAIR_N": "256", "OZGPU_BINS": "1"}),
+    ("plain plane stores", {"OZGPU_TMA_STORE": "0"}),
+    ("4-CTA clusters, B multicast", {"OZGPU_QUAD": "1", "OZGPU_BINS": "1"}),
     ("no lockstep", {"OZGPU_SYNC": "0", "OZGPU_BINS": "1"}),
     ("1-CTA B multicast", {"OZGPU_CTA_PAIR": "0"}),
     ("1-CTA plain", {"OZGPU_CTA_PAIR": "0", "OZGPU_MC": "0", "OZGPU_BINS": "1"}),
@@ -37,7 +40,7 @@ CASES = [
 def main():
     rng = np.random.default_rng(1)
     cfg = oz.MmaConfig.int8_int32()
-    m, k, n = 520, 384, 300
+    m, k, n = 1040, 384, 1100
     a = -0.5 + rng.random((m, k))
     b = (-0.5 + rng.random((k, n))) * np.exp2(rng.integers(-20, 20, size=(k, n)))
     base = None
