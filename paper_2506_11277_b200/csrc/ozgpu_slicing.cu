@@ -186,10 +186,13 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(
 // truncate mode (extract_field, slicing.cpp:35-45).
 // ----------------------------------------------------------------------------
 
-template <int T, bool CS = false>
-__device__ __forceinline__ void emit8_trunc_i8(const double (&v)[8], int q, int count,
+// FC > 0: the slice count is a compile-time constant (the common counts get
+// their own instantiation: fully unrolled windows and constant store offsets)
+template <int T, bool CS = false, int FC = 0>
+__device__ __forceinline__ void emit8_trunc_i8(const double (&v)[8], int q, int count_rt,
                                                int8_t* __restrict__ out, int64_t plane,
                                                int64_t off) {
+  const int count = FC > 0 ? FC : count_rt;
   constexpr int SPW = 63 / T;  // slices per window
   constexpr int WB = SPW * T;  // window bits
   constexpr uint64_t WMASK = (WB == 64) ? ~0ULL : ((1ULL << WB) - 1);
@@ -213,7 +216,7 @@ __device__ __forceinline__ void emit8_trunc_i8(const double (&v)[8], int q, int 
     const int ex = biased ? static_cast<int>(biased) - 1023 : -1022;
     lsb[e] = q + 52 - ex;
   }
-  for (int j = 0; j * SPW < count; ++j) {
+  auto window = [&](int j) {
     uint64_t w[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
@@ -242,6 +245,12 @@ __device__ __forceinline__ void emit8_trunc_i8(const double (&v)[8], int q, int 
       else
         *reinterpret_cast<uint2*>(out + l * plane + off) = make_uint2(lo, hi);
     }
+  };
+  if constexpr (FC > 0) {
+#pragma unroll
+    for (int j = 0; j < (FC + SPW - 1) / SPW; ++j) window(j);
+  } else {
+    for (int j = 0; j * SPW < count; ++j) window(j);
   }
 }
 
@@ -308,7 +317,7 @@ __global__ void __launch_bounds__(256) rowmax_kernel(const double* __restrict__ 
   }
 }
 
-template <int T, bool VEC, int MINB>
+template <int T, bool VEC, int MINB, int FC = 0>
 __global__ void __launch_bounds__(256, MINB) slice_rows_stream_kernel(
     const double* __restrict__ a, int64_t lda, int64_t m, int64_t k, int64_t kp, int64_t plane,
     int count, const int* __restrict__ scales, int8_t* __restrict__ out) {
@@ -332,14 +341,14 @@ __global__ void __launch_bounds__(256, MINB) slice_rows_stream_kernel(
 #pragma unroll
       for (int e = 0; e < 8; ++e) v[e] = j0 + e < k ? __ldcs(ar + j0 + e) : 0.0;
     }
-    emit8_trunc_i8<T>(v, __ldg(scales + row), count, out, plane, row * kp + j0);
+    emit8_trunc_i8<T, false, FC>(v, __ldg(scales + row), count, out, plane, row * kp + j0);
   }
 }
 
 // 128 (k) x 32 (n) tile transpose-and-slice into K-major [l][n][kp] int8.
 // Smem holds the tile column-major in 16-byte units with an XOR swizzle so
 // both the row-wise fill and the 8-entry column reads are conflict-light.
-template <int T>
+template <int T, int FC = 0>
 __global__ void __launch_bounds__(256) slice_cols_fast_kernel(
     const double* __restrict__ b, int64_t ldb, int64_t k, int64_t n, int64_t kp, int64_t plane,
     int count,
@@ -391,7 +400,7 @@ __global__ void __launch_bounds__(256) slice_cols_fast_kernel(
       v[2 * u] = t2.x;
       v[2 * u + 1] = t2.y;
     }
-    emit8_trunc_i8<T>(v, q, count, out, plane, col * kp + kk);
+    emit8_trunc_i8<T, false, FC>(v, q, count, out, plane, col * kp + kk);
   }
 }
 
@@ -794,6 +803,53 @@ static inline int grid_for(int64_t work, int per_block, int cap = 148 * 16) {
   return static_cast<int>(g < cap ? g : cap);
 }
 
+// OZGPU_SLICE_FC=0: runtime slice count everywhere (A/B of the instantiations)
+static bool fixed_counts() {
+  const char* env = std::getenv("OZGPU_SLICE_FC");
+  return !(env && std::atoi(env) == 0);
+}
+
+template <int T, int FC>
+static void rows_fc(int grid2, cudaStream_t st, const double* a, int64_t lda, int64_t m, int64_t k,
+                    int64_t kp, int64_t plane, const int* scales, int8_t* out) {
+  slice_rows_stream_kernel<T, true, 4, FC><<<grid2, 256, 0, st>>>(a, lda, m, k, kp, plane, FC,
+                                                                  scales, out);
+}
+
+template <int T>
+static void launch_rows_fc(int count, int grid2, cudaStream_t st, const double* a, int64_t lda,
+                           int64_t m, int64_t k, int64_t kp, int64_t plane, const int* scales,
+                           int8_t* out) {
+  switch (count) {
+#define OZ_FC(c) case c: rows_fc<T, c>(grid2, st, a, lda, m, k, kp, plane, scales, out); break;
+    OZ_FC(1) OZ_FC(2) OZ_FC(3) OZ_FC(4) OZ_FC(5) OZ_FC(6) OZ_FC(7) OZ_FC(8) OZ_FC(9)
+    OZ_FC(10) OZ_FC(11) OZ_FC(12) OZ_FC(13) OZ_FC(14) OZ_FC(15) OZ_FC(16) OZ_FC(17)
+#undef OZ_FC
+    default: break;
+  }
+}
+
+template <int T, int FC>
+static void cols_fc(dim3 grid, cudaStream_t st, const double* b, int64_t ldb, int64_t k, int64_t n,
+                    int64_t kp, int64_t plane, const unsigned long long* colmax, int8_t* out,
+                    int* scales) {
+  slice_cols_fast_kernel<T, FC><<<grid, 256, 0, st>>>(b, ldb, k, n, kp, plane, FC, colmax, out,
+                                                      scales);
+}
+
+template <int T>
+static bool launch_cols_fc(int count, dim3 grid, cudaStream_t st, const double* b, int64_t ldb,
+                           int64_t k, int64_t n, int64_t kp, int64_t plane,
+                           const unsigned long long* colmax, int8_t* out, int* scales) {
+  switch (count) {
+#define OZ_FC(c) case c: cols_fc<T, c>(grid, st, b, ldb, k, n, kp, plane, colmax, out, scales); return true;
+    OZ_FC(1) OZ_FC(2) OZ_FC(3) OZ_FC(4) OZ_FC(5) OZ_FC(6) OZ_FC(7) OZ_FC(8) OZ_FC(9)
+    OZ_FC(10) OZ_FC(11) OZ_FC(12) OZ_FC(13) OZ_FC(14) OZ_FC(15) OZ_FC(16) OZ_FC(17)
+#undef OZ_FC
+    default: return false;
+  }
+}
+
 template <int T>
 static int launch_rows_fast_t(const double* a, int64_t lda, int64_t m, int64_t k, int64_t kp,
                                int64_t plane, int count, int8_t* out, int* scales, int* status,
@@ -806,7 +862,15 @@ static int launch_rows_fast_t(const double* a, int64_t lda, int64_t m, int64_t k
   const bool four = !(mb && std::atoi(mb) == 1);
   if (vec) {
     rowmax_kernel<true><<<grid, 256, 0, st>>>(a, lda, m, k, scales, status);
-    if (four)
+    bool done = false;
+    if constexpr (T == 7) {
+      if (four && fixed_counts() && count >= 1 && count <= 17) {
+        launch_rows_fc<T>(count, grid2, st, a, lda, m, k, kp, plane, scales, out);
+        done = true;
+      }
+    }
+    if (done) {
+    } else if (four)
       slice_rows_stream_kernel<T, true, 4><<<grid2, 256, 0, st>>>(a, lda, m, k, kp, plane, count,
                                                                   scales, out);
     else
@@ -825,6 +889,11 @@ static void launch_cols_fast_t(const double* b, int64_t ldb, int64_t k, int64_t 
                                int64_t plane, int count, const unsigned long long* colmax,
                                int8_t* out, int* scales, cudaStream_t st) {
   dim3 grid(static_cast<unsigned>((kp + 127) / 128), static_cast<unsigned>((n + 31) / 32));
+  if constexpr (T == 7) {
+    if (fixed_counts() &&
+        launch_cols_fc<T>(count, grid, st, b, ldb, k, n, kp, plane, colmax, out, scales))
+      return;
+  }
   slice_cols_fast_kernel<T><<<grid, 256, 0, st>>>(b, ldb, k, n, kp, plane, count, colmax, out,
                                                   scales);
 }
