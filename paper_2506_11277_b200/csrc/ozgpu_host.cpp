@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <condition_variable>
 #include <cstring>
+#include <functional>
 #include <limits>
 #include <memory>
 #include <mutex>
@@ -134,6 +135,75 @@ struct PinnedBuf {
   }
 };
 
+// A persistent fork-join pool for the host-side staging copies (one per
+// context): run(nt, fn) calls fn(0..nt-1) on nt threads (the caller is one
+// of them) and returns when all are done.
+class CopyPool {
+ public:
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      quit_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  template <class F>
+  void run(int nt, F&& fn) {
+    if (nt <= 1) {
+      fn(0);
+      return;
+    }
+    ensure(nt - 1);
+    std::function<void(int)> task(std::forward<F>(fn));
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      task_ = &task;
+      parts_ = nt;
+      next_ = 1;
+      pending_ = nt - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    task(0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return pending_ == 0; });
+    task_ = nullptr;
+  }
+
+ private:
+  void ensure(int n) {
+    while (static_cast<int>(workers_.size()) < n) workers_.emplace_back([this] { loop(); });
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      std::function<void(int)>* task = nullptr;
+      int part = -1;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return quit_ || (gen_ != seen && task_ && next_ < parts_); });
+        if (quit_) return;
+        part = next_++;
+        if (next_ >= parts_) seen = gen_;
+        task = task_;
+      }
+      (*task)(part);
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (--pending_ == 0) done_cv_.notify_all();
+      }
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  std::function<void(int)>* task_ = nullptr;
+  int parts_ = 0, next_ = 0, pending_ = 0;
+  uint64_t gen_ = 0;
+  bool quit_ = false;
+};
+
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -175,7 +245,8 @@ struct ozgpu_ctx {
   cudaEvent_t fork_ev[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> pipe_events;
   // pinned staging of pageable host A / B / C (ozgpu_dgemm)
-  ozgpu::PinnedBuf stage_a, stage_b, stage_c, status_host;
+  ozgpu::PinnedBuf stage_a, stage_b, stage_c;
+  ozgpu::CopyPool copy_pool;  // staging copies (pageable <-> pinned)
   // Workspace ordering across streams: every call that touches the
   // workspace first makes its stream wait on ws_done (recorded where the
   // previous call's last use of the workspace was enqueued), and records it
@@ -1207,6 +1278,37 @@ bool is_pageable(const void* ptr) {
   return at.type == cudaMemoryTypeUnregistered;
 }
 
+// rows x cols doubles copied on the context's pool with `nt` threads; the
+// copy also ORs the clean-input status bits of every value it moves (1 =
+// Inf / NaN, 2 = -0, the GPU slicer's definition, matrix.cpp:22-29) into
+// *dirty, so a staged call knows its inputs' verdict on the host as soon as
+// they are staged.
+void pool_copy_check(CopyPool& pool, int nt, double* dst, int64_t ldd, const double* src,
+                     int64_t lds, int64_t rows, int64_t cols, std::atomic<int>* dirty) {
+  if (rows == 0 || cols == 0) return;
+  nt = static_cast<int>(std::clamp<int64_t>(nt, 1, rows));
+  pool.run(nt, [&](int t) {
+    const int64_t r0 = rows * t / nt, r1 = rows * (t + 1) / nt;
+    uint64_t bad_inf = 0, bad_negz = 0;
+    for (int64_t r = r0; r < r1; ++r) {
+      const uint64_t* in = reinterpret_cast<const uint64_t*>(src + r * lds);
+      uint64_t* out = reinterpret_cast<uint64_t*>(dst + r * ldd);
+      if (dirty) {
+        for (int64_t j = 0; j < cols; ++j) {
+          const uint64_t x = in[j];
+          out[j] = x;
+          bad_inf |= static_cast<uint64_t>((x & 0x7FF0000000000000ULL) == 0x7FF0000000000000ULL);
+          bad_negz |= static_cast<uint64_t>(x == 0x8000000000000000ULL);
+        }
+      } else {
+        std::memcpy(out, in, static_cast<size_t>(cols) * 8);
+      }
+    }
+    if (dirty && (bad_inf | bad_negz))
+      dirty->fetch_or((bad_inf ? 1 : 0) | (bad_negz ? 2 : 0));
+  });
+}
+
 // rows x cols doubles between strided host buffers, rows split over threads
 // (one per 16 MiB up to min(cores, 16); `threads` > 0 forces the count)
 void parallel_copy(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
@@ -1397,6 +1499,7 @@ void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const
     // waits only for its own block.
     std::atomic<size_t> staged{0};
     std::atomic<bool> stop_staging{false};
+    std::atomic<int> host_dirty{0};  // clean-input bits seen by the staging copies
     std::mutex stage_mu;
     std::condition_variable stage_cv;
     std::thread stager;
@@ -1408,11 +1511,12 @@ void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const
         for (size_t q = 0; q < arrivals.size() && !stop_staging.load(); ++q) {
           const size_t x = arrivals[q].second;
           if (arrivals[q].first == 'A')
-            parallel_copy(const_cast<double*>(a) + rb[x] * lda, lda, hs->a + rb[x] * hs->lda,
-                          hs->lda, rb[x + 1] - rb[x], k, stage_threads);
+            pool_copy_check(ctx->copy_pool, stage_threads, const_cast<double*>(a) + rb[x] * lda,
+                            lda, hs->a + rb[x] * hs->lda, hs->lda, rb[x + 1] - rb[x], k,
+                            &host_dirty);
           else
-            parallel_copy(const_cast<double*>(b) + cb[x], ldb, hs->b + cb[x], hs->ldb, k,
-                          cb[x + 1] - cb[x], stage_threads);
+            pool_copy_check(ctx->copy_pool, stage_threads, const_cast<double*>(b) + cb[x], ldb,
+                            hs->b + cb[x], hs->ldb, k, cb[x + 1] - cb[x], &host_dirty);
           {
             std::lock_guard<std::mutex> lk(stage_mu);
             staged.store(q + 1);
@@ -1457,19 +1561,6 @@ void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const
     if (!rect)
       for (auto& ar : arrivals) ar.first == 'A' ? copy_a(ar.second) : copy_b(ar.second);
     int64_t launches = 0;
-    // staged call: the input-status flag is read right after the last
-    // slicing kernel, so C blocks can be unstaged while later GEMMs run
-    // (and never reach the caller's C when the inputs are rejected)
-    size_t slices_done = 0;
-    cudaEvent_t status_ev = nullptr;
-    int* status_pinned = hs ? static_cast<int*>(ctx->status_host.get(sizeof(int))) : nullptr;
-    if (hs && !status_pinned) throw DeviceError("page-locked status word unavailable");
-    auto after_slice = [&]() {
-      if (!hs || ++slices_done != nr + nc) return;
-      OZ_CUDA(cudaMemcpyAsync(status_pinned, status, sizeof(int), cudaMemcpyDeviceToHost, st));
-      status_ev = next_event();
-      OZ_CUDA(cudaEventRecord(status_ev, st));
-    };
     struct CBlock {
       int64_t r0, r1, c0, c1;
       cudaEvent_t back;
@@ -1489,7 +1580,6 @@ void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const
                                   p.mode, slA + rb[i] * kp, 0, qa + rb[i], status, st, &launches,
                                   m * kp));
       mark("slice A" + std::to_string(i), st);
-      after_slice();
     };
     auto block = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1) {
       Presliced pre{slA + r0 * kp, m * kp, qa + r0, slB + c0 * kp, n * kp, qb + c0, kp};
@@ -1522,7 +1612,6 @@ void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const
         OZ_CUDA(launch_slice_cols(db + k * cb[j], nj, k, nj, kp, t, p.slices_b, p.mode,
                                   slB + cb[j] * kp, 0, qb + cb[j], colmax + cb[j], status, st,
                                   &launches, n * kp));
-      after_slice();
     };
     if (rect) {
       size_t na = 0, nbp = 0;  // A blocks / B panels sliced so far
@@ -1571,13 +1660,17 @@ void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const
     }
     ctx->launches += launches;
     if (hs) {
-      // unstage C block by block as each lands, once the inputs are known clean
-      OZ_CUDA(cudaEventSynchronize(status_ev));
-      if (*status_pinned == 0)
+      // Unstage C block by block as each lands, once the inputs are known
+      // clean: the staging copies checked every input value on the host, so
+      // the verdict is in as soon as the last block is staged (the GPU's own
+      // status, read below, must agree).
+      wait_staged(arrivals.size() - 1);
+      if (host_dirty.load() == 0)
         for (const CBlock& cbk : cblocks) {
           OZ_CUDA(cudaEventSynchronize(cbk.back));
-          parallel_copy(hs->c + cbk.r0 * hs->ldc + cbk.c0, hs->ldc, c + cbk.r0 * ldc + cbk.c0,
-                        ldc, cbk.r1 - cbk.r0, cbk.c1 - cbk.c0, stage_threads);
+          pool_copy_check(ctx->copy_pool, stage_threads, hs->c + cbk.r0 * hs->ldc + cbk.c0,
+                          hs->ldc, c + cbk.r0 * ldc + cbk.c0, ldc, cbk.r1 - cbk.r0,
+                          cbk.c1 - cbk.c0, nullptr);
         }
     }
     int hs_status = 0;
@@ -1593,6 +1686,8 @@ void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const
       }
       for (auto& mk : marks) cudaEventDestroy(mk.second);
     }
+    if (hs && (hs_status != 0) != (host_dirty.load() != 0))
+      throw std::logic_error("multiply: host and device input checks disagree");
     if (hs_status)
       throw std::invalid_argument("multiply: inputs must be finite with no negative zeros");
     if (diag) *diag = make_diag(p, cfg, m, n, k, 0);
