@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <unistd.h>
+#include <immintrin.h>
 
 #include <algorithm>
 #include <map>
@@ -1283,29 +1284,60 @@ bool is_pageable(const void* ptr) {
 // Inf / NaN, 2 = -0, the GPU slicer's definition, matrix.cpp:22-29) into
 // *dirty, so a staged call knows its inputs' verdict on the host as soon as
 // they are staged.
+// One row: copy + status bits.  AVX2 when the CPU has it (streaming stores:
+// the pinned destination is read next by the DMA engine, not by the CPU).
+int copy_check_scalar(uint64_t* out, const uint64_t* in, int64_t n) {
+  uint64_t bi = 0, bz = 0;
+  for (int64_t j = 0; j < n; ++j) {
+    const uint64_t x = in[j];
+    out[j] = x;
+    bi |= static_cast<uint64_t>((x & 0x7FF0000000000000ULL) == 0x7FF0000000000000ULL);
+    bz |= static_cast<uint64_t>(x == 0x8000000000000000ULL);
+  }
+  return (bi ? 1 : 0) | (bz ? 2 : 0);
+}
+
+__attribute__((target("avx2"))) int copy_check_avx2(uint64_t* out, const uint64_t* in,
+                                                     int64_t n) {
+  int64_t j = 0;
+  int bits = 0;
+  while (j < n && (reinterpret_cast<uintptr_t>(out + j) & 31)) {
+    bits |= copy_check_scalar(out + j, in + j, 1);
+    ++j;
+  }
+  const __m256i em = _mm256_set1_epi64x(0x7FF0000000000000LL);
+  const __m256i nz = _mm256_set1_epi64x(static_cast<long long>(0x8000000000000000ULL));
+  __m256i acc_i = _mm256_setzero_si256(), acc_z = _mm256_setzero_si256();
+  for (; j + 4 <= n; j += 4) {
+    const __m256i x = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(in + j));
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(out + j), x);
+    acc_i = _mm256_or_si256(acc_i, _mm256_cmpeq_epi64(_mm256_and_si256(x, em), em));
+    acc_z = _mm256_or_si256(acc_z, _mm256_cmpeq_epi64(x, nz));
+  }
+  if (j < n) bits |= copy_check_scalar(out + j, in + j, n - j);
+  _mm_sfence();
+  if (!_mm256_testz_si256(acc_i, acc_i)) bits |= 1;
+  if (!_mm256_testz_si256(acc_z, acc_z)) bits |= 2;
+  return bits;
+}
+
 void pool_copy_check(CopyPool& pool, int nt, double* dst, int64_t ldd, const double* src,
                      int64_t lds, int64_t rows, int64_t cols, std::atomic<int>* dirty) {
   if (rows == 0 || cols == 0) return;
   nt = static_cast<int>(std::clamp<int64_t>(nt, 1, rows));
+  static const bool avx2 = __builtin_cpu_supports("avx2");
   pool.run(nt, [&](int t) {
     const int64_t r0 = rows * t / nt, r1 = rows * (t + 1) / nt;
-    uint64_t bad_inf = 0, bad_negz = 0;
+    int bits = 0;
     for (int64_t r = r0; r < r1; ++r) {
       const uint64_t* in = reinterpret_cast<const uint64_t*>(src + r * lds);
       uint64_t* out = reinterpret_cast<uint64_t*>(dst + r * ldd);
-      if (dirty) {
-        for (int64_t j = 0; j < cols; ++j) {
-          const uint64_t x = in[j];
-          out[j] = x;
-          bad_inf |= static_cast<uint64_t>((x & 0x7FF0000000000000ULL) == 0x7FF0000000000000ULL);
-          bad_negz |= static_cast<uint64_t>(x == 0x8000000000000000ULL);
-        }
-      } else {
+      if (dirty)
+        bits |= avx2 ? copy_check_avx2(out, in, cols) : copy_check_scalar(out, in, cols);
+      else
         std::memcpy(out, in, static_cast<size_t>(cols) * 8);
-      }
     }
-    if (dirty && (bad_inf | bad_negz))
-      dirty->fetch_or((bad_inf ? 1 : 0) | (bad_negz ? 2 : 0));
+    if (dirty && bits) dirty->fetch_or(bits);
   });
 }
 
