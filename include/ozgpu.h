@@ -237,6 +237,23 @@ int ozgpu_dgemm_device(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const do
                        int64_t lda, const double* b, int64_t ldb, double* c, int64_t ldc,
                        ozgpu_mma_config cfg, const ozgpu_plan* plan, void* stream,
                        int* dev_status, ozgpu_diag* diag);
+/* Device-resident sharding over the GPUs of the node (the
+ * reference has no multi-device path -- scheme.cpp:219 is its one entry).
+ * a, b, c are device pointers on src_device; C is split into the p_r x p_c
+ * blocks of ozgpu_dgemm_multi.  A context on another device pulls its A
+ * row-panel and B column-panel over NVLink (cudaMemcpy3DPeerAsync, peer
+ * access enabled on first use), multiplies on its own stream and pushes its
+ * C block back; a context on src_device reads its panels in place.  The work
+ * is ordered after `stream` (a cudaStream_t on src_device) and `stream`
+ * waits for every block, so the call returns without synchronising, like
+ * ozgpu_dgemm_device.  dev_status: NULL or `count` device ints on
+ * src_device, one per block (0 ok, nonzero: that block saw Inf / NaN / -0).
+ * Bit-identical to ozgpu_dgemm_device. */
+int ozgpu_dgemm_device_multi(ozgpu_ctx* const* ctxs, int count, int src_device, int64_t m,
+                             int64_t n, int64_t k, const double* a, int64_t lda, const double* b,
+                             int64_t ldb, double* c, int64_t ldc, ozgpu_mma_config cfg,
+                             const ozgpu_plan* plan, void* stream, int* dev_status,
+                             ozgpu_diag* diag);
 
 /* ---- debug hooks (bit-exact against the reference) --------------------- */
 /* split_rows / split_cols, proj/src/slicing.cpp:67-132, on the GPU.

@@ -539,6 +539,33 @@ def multiply_device(m: int, n: int, k: int, a_ptr: int, lda: int, b_ptr: int, ld
     return Diagnostics._from_c(d)
 
 
+_sig("ozgpu_dgemm_device_multi", ctypes.c_int, ctypes.POINTER(_P), ctypes.c_int, ctypes.c_int,
+     _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64, _Cfg, ctypes.POINTER(_Plan), _P, _P,
+     ctypes.POINTER(_Diag))
+
+
+def multiply_device_multi(m: int, n: int, k: int, a_ptr: int, lda: int, b_ptr: int, ldb: int,
+                          c_ptr: int, ldc: int, cfg: MmaConfig, plan: MultiplyPlan,
+                          devices: List[int], src_device: int = 0, stream: int = 0,
+                          status_ptr: int = 0) -> Diagnostics:
+    """Device-resident multiply sharded in 2-D C tiles over `devices`
+    (ozgpu_dgemm_device_multi): A / B / C live on `src_device`, remote
+    contexts pull their panels over NVLink and push their C block back.
+    Ordered on `stream` (of src_device), no sync; `status_ptr`: 0 or
+    len(devices) device ints on src_device, one per block."""
+    if not devices:
+        raise InvalidArgument("multiply_device_multi: no devices")
+    arr = (ctypes.c_int * len(devices))(*devices)
+    ctxs = (_P * len(devices))()
+    _check(_lib.ozgpu_device_contexts(arr, len(devices), ctxs))
+    d = _Diag()
+    pc = plan._c()
+    _check(_lib.ozgpu_dgemm_device_multi(ctxs, len(devices), src_device, m, n, k, a_ptr, lda,
+                                         b_ptr, ldb, c_ptr, ldc, cfg._c(), ctypes.byref(pc),
+                                         stream or None, status_ptr or None, ctypes.byref(d)))
+    return Diagnostics._from_c(d)
+
+
 # ------------------------------------------------------------ debug hooks
 
 

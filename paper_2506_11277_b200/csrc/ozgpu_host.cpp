@@ -23,6 +23,7 @@
 #include <limits>
 #include <memory>
 #include <mutex>
+#include <set>
 #include <thread>
 #include <random>
 #include <string>
@@ -256,6 +257,12 @@ struct ozgpu_ctx {
   // path on ctx->stream) could overwrite slices / planes still in use.
   cudaEvent_t ws_done = nullptr;
   bool ws_recorded = false;
+  // ozgpu_dgemm_device_multi: this context's stream, and its A row-panel,
+  // B column-panel, C block and status int when the operands live on
+  // another device (pulled / pushed over NVLink by peer copies)
+  std::mutex multi_mu;
+  cudaStream_t multi_stream = nullptr;
+  ozgpu::DevBuf peer_a, peer_b, peer_c, peer_status;
   // debug hook ozgpu_pair_planes: run_multiply stops after the pair GEMM
   // (split mode, no row blocking) and leaves the int32 chunk planes in
   // `planes` with this geometry
@@ -1869,6 +1876,10 @@ int ozgpu_destroy(ozgpu_ctx* ctx) {
       cudaStreamDestroy(ctx->d2h_stream);
     }
     for (cudaEvent_t e : ctx->pipe_events) cudaEventDestroy(e);
+    if (ctx->multi_stream) {
+      cudaStreamSynchronize(ctx->multi_stream);
+      cudaStreamDestroy(ctx->multi_stream);
+    }
     if (ctx->fork_stream) {
       cudaStreamSynchronize(ctx->fork_stream);
       cudaStreamDestroy(ctx->fork_stream);
@@ -2413,6 +2424,62 @@ int ozgpu_device_contexts(const int* devices, int count, ozgpu_ctx** out) {
   });
 }
 
+namespace ozgpu {
+namespace {
+
+// p_r >= p_c, p_r * p_c == count, as square as possible (1x1, 2x1, 2x2, 4x2)
+void shard_grid(int count, int& pr, int& pc) {
+  pr = count;
+  pc = 1;
+  for (int q = 1; q <= count; ++q)
+    if (count % q == 0 && count / q >= q) {
+      pr = count / q;
+      pc = q;
+    }
+}
+
+void shard_range(int64_t len, int parts, int idx, int64_t& lo, int64_t& hi) {
+  const int64_t base = len / parts, rem = len % parts;
+  lo = idx * base + std::min<int64_t>(idx, rem);
+  hi = lo + base + (idx < rem ? 1 : 0);
+}
+
+// Pitched copy of a rows x width_bytes window between (possibly different)
+// devices: NVLink P2P when peer access is on, a device-to-device copy when
+// both sides are the same device.
+void peer_copy_2d(void* dst, size_t dpitch, int ddev, const void* src, size_t spitch, int sdev,
+                  size_t width_bytes, size_t rows, cudaStream_t st) {
+  if (!width_bytes || !rows) return;
+  cudaMemcpy3DPeerParms p{};
+  p.srcPtr = make_cudaPitchedPtr(const_cast<void*>(src), spitch, width_bytes, rows);
+  p.srcDevice = sdev;
+  p.dstPtr = make_cudaPitchedPtr(dst, dpitch, width_bytes, rows);
+  p.dstDevice = ddev;
+  p.extent = make_cudaExtent(width_bytes, rows, 1);
+  OZ_CUDA(cudaMemcpy3DPeerAsync(&p, st));
+}
+
+void enable_peer(int from, int to) {
+  if (from == to) return;
+  static std::mutex mu;
+  static std::set<std::pair<int, int>> done;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!done.insert({from, to}).second) return;
+  int can = 0;
+  OZ_CUDA(cudaDeviceCanAccessPeer(&can, from, to));
+  if (!can) return;  // the copies still work, staged by the driver
+  int cur = 0;
+  OZ_CUDA(cudaGetDevice(&cur));
+  OZ_CUDA(cudaSetDevice(from));
+  cudaError_t e = cudaDeviceEnablePeerAccess(to, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+  else OZ_CUDA(e);
+  OZ_CUDA(cudaSetDevice(cur));
+}
+
+}  // namespace
+}  // namespace ozgpu
+
 // 2-D C-tile sharding of one host-pointer multiply over several contexts
 // (SURVEY.md 8e): context r computes C block (i, j) = divmod(r, p_c) with the
 // full k from its A row-panel and B column-panel, pulled from the caller's
@@ -2431,23 +2498,11 @@ int ozgpu_dgemm_multi(ozgpu_ctx* const* ctxs, int count, int64_t m, int64_t n, i
       if (!ctxs[r]) throw std::invalid_argument("multiply: null context");
     check_plan(plan);
     check_operands("multiply", m, n, k, a, lda, b, ldb, c, ldc);
-    // p_r >= p_c, p_r * p_c == count, as square as possible (1x1, 2x1, 2x2, 4x2)
-    pr = count;
-    pc = 1;
-    for (int q = 1; q <= count; ++q)
-      if (count % q == 0 && count / q >= q) {
-        pr = count / q;
-        pc = q;
-      }
+    shard_grid(count, pr, pc);
   });
   if (rc != OZGPU_OK) return rc;
   if (count == 1 || m < pr || n < pc)  // nothing to shard (every block must be non-empty)
     return ozgpu_dgemm(ctxs[0], m, n, k, a, lda, b, ldb, c, ldc, cfg, plan, diag);
-  auto split = [](int64_t len, int parts, int idx, int64_t& lo, int64_t& hi) {
-    const int64_t base = len / parts, rem = len % parts;
-    lo = idx * base + std::min<int64_t>(idx, rem);
-    hi = lo + base + (idx < rem ? 1 : 0);
-  };
   std::vector<int> codes(count, OZGPU_OK);
   std::vector<std::string> msgs(count);
   std::vector<ozgpu_diag> diags(count);
@@ -2455,8 +2510,8 @@ int ozgpu_dgemm_multi(ozgpu_ctx* const* ctxs, int count, int64_t m, int64_t n, i
   for (int r = 0; r < count; ++r)
     pool.emplace_back([&, r] {
       int64_t r0, r1, c0, c1;
-      split(m, pr, r / pc, r0, r1);
-      split(n, pc, r % pc, c0, c1);
+      shard_range(m, pr, r / pc, r0, r1);
+      shard_range(n, pc, r % pc, c0, c1);
       codes[r] = ozgpu_dgemm(ctxs[r], r1 - r0, c1 - c0, k, a + r0 * lda, lda, b + c0, ldb,
                              c + r0 * ldc + c0, ldc, cfg, plan, &diags[r]);
       if (codes[r] != OZGPU_OK) msgs[r] = g_error;  // thread-local: copy out
@@ -2472,6 +2527,118 @@ int ozgpu_dgemm_multi(ozgpu_ctx* const* ctxs, int count, int64_t m, int64_t n, i
     for (const auto& d : diags) psi = std::max(psi, d.realized_psi);
     if (diag) *diag = make_diag(*plan, cfg, m, n, k, psi);
   });
+}
+
+
+// Device-resident 2-D C-tile sharding: A, B and C live on
+// src_device; context r computes C block (r / p_c, r % p_c) with the full k.
+// A context on another device pulls its A row-panel and B column-panel over
+// NVLink (peer copies), multiplies on its own stream and pushes its C block
+// back; a context on src_device reads the panels in place.  Only the panels
+// a block needs move, once each -- no collective, since scales are per row
+// of A / column of B and every block is independent (bit-identical to
+// ozgpu_dgemm_device).  Ordered after the caller's stream and before its
+// later work by events; the call does not synchronise.
+int ozgpu_dgemm_device_multi(ozgpu_ctx* const* ctxs, int count, int src_device, int64_t m,
+                             int64_t n, int64_t k, const double* a, int64_t lda, const double* b,
+                             int64_t ldb, double* c, int64_t ldc, ozgpu_mma_config cfg,
+                             const ozgpu_plan* plan, void* stream, int* dev_status,
+                             ozgpu_diag* diag) {
+  int pr = 1, pc = 1;
+  bool force_peer = false;
+  int rc = guarded([&] {
+    if (!ctxs || count < 1) throw std::invalid_argument("multiply: no contexts");
+    for (int r = 0; r < count; ++r)
+      if (!ctxs[r]) throw std::invalid_argument("multiply: null context");
+    check_plan(plan);
+    check_operands("multiply", m, n, k, a, lda, b, ldb, c, ldc);
+    if (k < 1) throw std::invalid_argument("multiply: empty inner dimension");
+    int ndev = 0;
+    OZ_CUDA(cudaGetDeviceCount(&ndev));
+    if (src_device < 0 || src_device >= ndev)
+      throw std::invalid_argument("multiply: bad source device");
+    shard_grid(count, pr, pc);
+    // test hook: treat contexts on src_device as remote (exercises the
+    // panel copies on a one-GPU box)
+    const char* fe = std::getenv("OZGPU_MULTI_PEER");
+    force_peer = fe && std::string(fe) == "1";
+  });
+  if (rc != OZGPU_OK) return rc;
+  if (m < pr || n < pc) {  // every block must be non-empty: one context does it all
+    count = 1;
+    pr = pc = 1;
+  }
+  std::vector<long long> psi(count, 0);
+  int failed = OZGPU_OK;
+  rc = guarded([&] {
+    cudaStream_t caller = static_cast<cudaStream_t>(stream);
+    OZ_CUDA(cudaSetDevice(src_device));
+    cudaEvent_t ready = nullptr;
+    OZ_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    std::unique_ptr<CUevent_st, decltype(&cudaEventDestroy)> ready_guard(ready, &cudaEventDestroy);
+    OZ_CUDA(cudaEventRecord(ready, caller));
+    for (int r = 0; r < count; ++r) {
+      ozgpu_ctx* x = ctxs[r];
+      int64_t r0, r1, c0, c1;
+      shard_range(m, pr, r / pc, r0, r1);
+      shard_range(n, pc, r % pc, c0, c1);
+      const int64_t rows = r1 - r0, cols = c1 - c0;
+      const bool local = x->device == src_device && !force_peer;
+      std::lock_guard<std::mutex> lock(x->multi_mu);
+      OZ_CUDA(cudaSetDevice(x->device));
+      if (!x->multi_stream) OZ_CUDA(cudaStreamCreateWithFlags(&x->multi_stream, cudaStreamNonBlocking));
+      cudaStream_t s = x->multi_stream;
+      OZ_CUDA(cudaStreamWaitEvent(s, ready, 0));
+      int* slot = dev_status ? dev_status + r : nullptr;
+      ozgpu_diag d{};
+      int code;
+      if (local) {
+        code = ozgpu_dgemm_device(x, rows, cols, k, a + r0 * lda, lda, b + c0, ldb,
+                                  c + r0 * ldc + c0, ldc, cfg, plan, s, slot, &d);
+      } else {
+        enable_peer(x->device, src_device);
+        enable_peer(src_device, x->device);
+        const size_t ba = sizeof(double) * rows * k, bb = sizeof(double) * k * cols,
+                     bc = sizeof(double) * rows * cols;
+        if (ba > x->peer_a.bytes || bb > x->peer_b.bytes || bc > x->peer_c.bytes)
+          OZ_CUDA(cudaStreamSynchronize(s));  // regrowing: earlier calls' panels in flight
+        auto* pa = static_cast<double*>(x->peer_a.get(ba));
+        auto* pb = static_cast<double*>(x->peer_b.get(bb));
+        auto* pcb = static_cast<double*>(x->peer_c.get(bc));
+        int* pst = slot ? static_cast<int*>(x->peer_status.get(sizeof(int))) : nullptr;
+        OZ_CUDA(cudaSetDevice(x->device));
+        peer_copy_2d(pa, sizeof(double) * k, x->device, a + r0 * lda, sizeof(double) * lda,
+                     src_device, sizeof(double) * k, rows, s);
+        peer_copy_2d(pb, sizeof(double) * cols, x->device, b + c0, sizeof(double) * ldb,
+                     src_device, sizeof(double) * cols, k, s);
+        code = ozgpu_dgemm_device(x, rows, cols, k, pa, k, pb, cols, pcb, cols, cfg, plan, s, pst,
+                                  &d);
+        if (code == OZGPU_OK) {
+          OZ_CUDA(cudaSetDevice(x->device));
+          peer_copy_2d(c + r0 * ldc + c0, sizeof(double) * ldc, src_device, pcb,
+                       sizeof(double) * cols, x->device, sizeof(double) * cols, rows, s);
+          if (slot) OZ_CUDA(cudaMemcpyPeerAsync(slot, src_device, pst, x->device, sizeof(int), s));
+        }
+      }
+      if (code != OZGPU_OK) {  // g_error already says why; blocks before it stay enqueued
+        failed = code;
+        cudaSetDevice(src_device);
+        return;
+      }
+      psi[r] = d.realized_psi;
+      // the caller's stream continues once this block (and its copies) is done
+      OZ_CUDA(cudaSetDevice(x->device));
+      cudaEvent_t done = nullptr;
+      OZ_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+      OZ_CUDA(cudaEventRecord(done, s));
+      cudaError_t we = cudaStreamWaitEvent(caller, done, 0);
+      cudaEventDestroy(done);  // released once it completes
+      OZ_CUDA(we);
+    }
+    OZ_CUDA(cudaSetDevice(src_device));
+    if (diag) *diag = make_diag(*plan, cfg, m, n, k, *std::max_element(psi.begin(), psi.end()));
+  });
+  return rc != OZGPU_OK ? rc : failed;
 }
 
 int ozgpu_split_i8(ozgpu_ctx* ctx, int orientation, int64_t rows, int64_t cols, const double* x,

@@ -139,3 +139,56 @@ def test_cpp_api_shards_over_ozgpu_devices(oz, ref):
     env = dict(os.environ, OZGPU_DEVICES="0,0")
     r = subprocess.run([exe], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-2000:])
+
+
+@pytest.mark.parametrize("peer", [0, 1])
+@pytest.mark.parametrize("slots", [[0, 0], [0, 0, 0, 0]])
+def test_device_sharded_multiply(oz, slots, peer, monkeypatch):
+    """ozgpu_dgemm_device_multi: device-resident A / B / C (strided, lda > k,
+    ldb > n, ldc > n) split in 2-D C tiles over extra contexts on the one
+    GPU.  peer=1 (OZGPU_MULTI_PEER) treats them as remote, so the panel pulls
+    and C-block pushes of the NVLink path run as device-to-device copies.
+    Bitwise the single-context result over eager / capture / replay calls,
+    ordered on the caller's stream without a host sync, the padding of C
+    untouched, and per-block input status."""
+    import torch
+    monkeypatch.setenv("OZGPU_MULTI_PEER", str(peer))
+    rng = np.random.default_rng(7 + len(slots))
+    cfg = oz.MmaConfig.int8_int32()
+    dev = torch.device("cuda:0")
+    m, k, n = 2100, 1100, 1700
+    a = uniform(m, k, rng)
+    b = random_matrix(k, n, rng, -10, 10, 0.02)
+    plan = oz.make_plan(cfg, k, 8, 8)
+    want = oz.multiply(a, b, cfg, plan)
+    A = torch.zeros(m, k + 40, dtype=torch.float64, device=dev)
+    B = torch.zeros(k, n + 24, dtype=torch.float64, device=dev)
+    A[:, :k] = torch.from_numpy(a)
+    B[:, :n] = torch.from_numpy(b)
+    C = torch.full((m, n + 8), 3.5, dtype=torch.float64, device=dev)
+    status = torch.full((len(slots),), -1, dtype=torch.int32, device=dev)
+    s = torch.cuda.Stream(device=dev)
+    torch.cuda.synchronize()
+    for it in range(3):
+        with torch.cuda.stream(s):
+            C[:, :n].fill_(0.0)
+        d = oz.multiply_device_multi(m, n, k, A.data_ptr(), k + 40, B.data_ptr(), n + 24,
+                                     C.data_ptr(), n + 8, cfg, plan, slots, src_device=0,
+                                     stream=s.cuda_stream, status_ptr=status.data_ptr())
+        with torch.cuda.stream(s):  # ordered after every block without a host sync
+            got = C.clone()
+            st = status.clone()
+        s.synchronize()
+        g = got.cpu().numpy()
+        assert bits_equal(np.ascontiguousarray(g[:, :n]), want.c), (it, mismatch_report(g[:, :n], want.c))
+        assert (g[:, n:] == 3.5).all()
+        assert st.cpu().tolist() == [0] * len(slots)
+        assert d == want.diagnostics
+    # a NaN in the last row of A dirties only the blocks of the last block row
+    A[m - 1, 5] = float("nan")
+    oz.multiply_device_multi(m, n, k, A.data_ptr(), k + 40, B.data_ptr(), n + 24, C.data_ptr(),
+                             n + 8, cfg, plan, slots, stream=s.cuda_stream,
+                             status_ptr=status.data_ptr())
+    s.synchronize()
+    flags = [v != 0 for v in status.cpu().tolist()]
+    assert flags == ([False, True] if len(slots) == 2 else [False, False, True, True])

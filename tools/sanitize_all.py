@@ -88,6 +88,24 @@ def main():
     big_b = -0.5 + rng.random((1536, 2048))
     oz.multiply(big_a, big_b, cfg, oz.make_plan(cfg, 1536, 6, 6))
     print("ok host pipeline", flush=True)
+    # validation tools: exact_gemm (error-free slices + full schedule), metrics
+    ex = oz.exact_gemm(a[:96], b[:, :80])
+    oz.max_elementwise_error(ex, ex)
+    oz.normwise_gemm_error(ex, ex, a[:96], b[:, :80], np.zeros_like(ex), 1.0, 0.0)
+    oz.min_exact_slices(a[:50], 7, oz.BlockOrientation.ROWS)
+    print("ok exact_gemm, metrics", flush=True)
+    # device-resident sharding with the peer-copy path (two contexts on one GPU)
+    import torch
+    os.environ["OZGPU_MULTI_PEER"] = "1"
+    dev = torch.device("cuda:0")
+    da, db = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    dc = torch.empty(m, n, dtype=torch.float64, device=dev)
+    st = torch.zeros(2, dtype=torch.int32, device=dev)
+    oz.multiply_device_multi(m, n, k, da.data_ptr(), k, db.data_ptr(), n, dc.data_ptr(), n, cfg,
+                             oz.make_plan(cfg, k, 6, 6), [0, 0], status_ptr=st.data_ptr())
+    torch.cuda.synchronize()
+    os.environ.pop("OZGPU_MULTI_PEER")
+    print("ok device multi (peer copies)", flush=True)
 
 
 if __name__ == "__main__":
