@@ -40,7 +40,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "lib", "libozgpu.so")
+_LIB_PATH = os.environ.get("OZGPU_LIB_OVERRIDE") or os.path.join(_HERE, "lib", "libozgpu.so")  # override: A/B tools
 
 
 def library_path() -> str:

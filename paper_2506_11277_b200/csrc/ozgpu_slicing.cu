@@ -186,12 +186,136 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(
 // truncate mode (extract_field, slicing.cpp:35-45).
 // ----------------------------------------------------------------------------
 
+// The t = 7 slicer with a known slice count (the production case), cut for
+// the integer ALU pipe, which bounds the slicing kernels (ncu: ALU 88 %,
+// issue 60 %):
+//  * the two 63-bit windows come from one pre-shifted significand:
+//    W0 = floor(|x| 2^(63-q)) = (sig << 10) >> a0 and L = the next 64 bits of
+//    (sig << 10):0 >> a0 (window 1 = L >> 1, so its digits sit one bit
+//    higher in L); the hidden bit and the subnormal exponent come from one
+//    max-and-add, sig_hi = |hi| - max(biased - 1, 0) * 2^20;
+//  * each digit is moved to its byte by a constant shift chosen per
+//    (digit, byte): left shifts compile to IMAD.SHL on the FMA pipe, and the
+//    mask and merge are one LOP3 (XOR-accumulate);
+//  * signs: the accumulator starts at m & 0x7F per negative byte, so after
+//    the merge a negative byte holds 127 - d; adding m & 0x01 (no carry
+//    leaves a byte: 127 - d + 1 <= 128) and XOR-ing m & 0x80 gives 256 - d.
+// Needs q >= -1000 (then a0 = 1021 + q - max(biased - 1, 0) >= 0 for every
+// entry |x| < 2^q); tinier blocks take emit8_trunc_i8.  Bit-identical to
+// emit8_trunc_i8<7> (and so to slice_of(), slicing.cpp:35-45).
+// x >> c for a constant 0 <= c < 32 as the high word of x * 2^(32-c): an
+// IMAD.HI on the FMA pipe, which the ALU-bound slicers leave mostly idle.
+__device__ __forceinline__ uint32_t shr_fma(uint32_t x, int c) {
+  if (c == 0) return x;
+  uint32_t r;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(1u << (32 - c)));
+  return r;
+}
+
+template <bool CS, int FC>
+__device__ __forceinline__ void emit8_t7(const double (&v)[8], int q, int8_t* __restrict__ out,
+                                         int64_t plane, int64_t off) {
+  static_assert(FC >= 1 && FC <= 18, "two 63-bit windows hold 18 slices");
+  constexpr bool kTwo = FC > 9;
+  constexpr bool kTwoLo = FC > 13;  // slices 9..12 sit in the high word of L
+  uint32_t w0h[8], w0l[8], lh[8], ll[8];
+  uint32_t hw[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const uint64_t bits = dbl_bits(v[e]);
+    hw[e] = static_cast<uint32_t>(bits >> 32);
+    const uint32_t habs = hw[e] & 0x7FFFFFFFu;
+    const int b1m1 = max(static_cast<int>(habs >> 20) - 1, 0);
+    const uint32_t sig_hi = habs - (static_cast<uint32_t>(b1m1) << 20);
+    const uint64_t sig10 = ((static_cast<uint64_t>(sig_hi) << 32) | static_cast<uint32_t>(bits)) << 10;
+    const uint32_t a0 = static_cast<uint32_t>(1021 + q - b1m1);
+    uint64_t w0;
+    asm("shr.b64 %0, %1, %2;" : "=l"(w0) : "l"(sig10), "r"(a0));
+    w0h[e] = static_cast<uint32_t>(w0 >> 32);
+    w0l[e] = static_cast<uint32_t>(w0);
+    if constexpr (kTwo) {
+      // a0 <= 64: sig10 << (64 - a0); a0 > 64: sig10 >> (a0 - 64).  The
+      // other shift's amount wraps past 64, which PTX clamps to a zero
+      // result, so an OR selects (both equal sig10 at a0 = 64).
+      if constexpr (kTwoLo) {
+        uint64_t left, right;
+        asm("shl.b64 %0, %1, %2;" : "=l"(left) : "l"(sig10), "r"(64u - a0));
+        asm("shr.b64 %0, %1, %2;" : "=l"(right) : "l"(sig10), "r"(a0 - 64u));
+        const uint64_t l = left | right;
+        lh[e] = static_cast<uint32_t>(l >> 32);
+        ll[e] = static_cast<uint32_t>(l);
+      } else {  // only the high word of L (its low word is dead code)
+        uint64_t left;
+        uint32_t right;
+        asm("shl.b64 %0, %1, %2;" : "=l"(left) : "l"(sig10), "r"(64u - a0));
+        asm("shr.b32 %0, %1, %2;" : "=r"(right) : "r"(static_cast<uint32_t>(sig10 >> 32)), "r"(a0 - 64u));
+        lh[e] = static_cast<uint32_t>(left >> 32) | right;
+        ll[e] = 0;
+      }
+    }
+  }
+  // per-byte sign masks of entries 0..3 / 4..7 (byte e = 0xFF if v[e] < 0)
+  uint32_t m[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    // prmt selector nibble 0xB / 0xF: byte 3 of the first / second source
+    // with its sign bit replicated over the byte
+    uint32_t t01, t23;
+    asm("prmt.b32 %0, %1, %2, 0x00FB;" : "=r"(t01) : "r"(hw[4 * h]), "r"(hw[4 * h + 1]));
+    asm("prmt.b32 %0, %1, %2, 0x00FB;" : "=r"(t23) : "r"(hw[4 * h + 2]), "r"(hw[4 * h + 3]));
+    m[h] = __byte_perm(t01, t23, 0x5410);
+  }
+  const uint32_t m7f[2] = {m[0] & 0x7F7F7F7Fu, m[1] & 0x7F7F7F7Fu};
+  const uint32_t m01[2] = {m[0] & 0x01010101u, m[1] & 0x01010101u};
+  const uint32_t m80[2] = {m[0] & 0x80808080u, m[1] & 0x80808080u};
+  int8_t* base = out + off;
+#pragma unroll
+  for (int l = 0; l < FC; ++l) {
+    const int j = l / 9, i = l % 9;
+    const int P = 56 - 7 * i + j;  // digit bit position in its 64-bit window
+    uint32_t word[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint32_t acc = m7f[h];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int e = 4 * h + b;
+        const uint32_t hi = j ? lh[e] : w0h[e], lo = j ? ll[e] : w0l[e];
+        uint32_t src;
+        if (P >= 32) {
+          const int p = P - 32;
+          src = p >= 8 * b ? shr_fma(hi, p - 8 * b) : hi << (8 * b - p);
+        } else if (P + 7 <= 32) {
+          src = P >= 8 * b ? shr_fma(lo, P - 8 * b) : lo << (8 * b - P);
+        } else {  // straddles the halves: funnel shift
+          src = __funnelshift_r(lo, hi, P - 8 * b);
+        }
+        // acc = (src & mask) ^ acc as one explicit LOP3 (left to itself the
+        // compiler masks the first byte and XORs m7f in as extra ops)
+        asm("lop3.b32 %0, %1, %2, %0, 0x6A;" : "+r"(acc) : "r"(src), "r"(0x7Fu << (8 * b)));
+      }
+      word[h] = (acc + m01[h]) ^ m80[h];
+    }
+    int8_t* dst = base + l * plane;
+    if constexpr (CS)
+      __stcs(reinterpret_cast<uint2*>(dst), make_uint2(word[0], word[1]));
+    else
+      *reinterpret_cast<uint2*>(dst) = make_uint2(word[0], word[1]);
+  }
+}
+
 // FC > 0: the slice count is a compile-time constant (the common counts get
 // their own instantiation: fully unrolled windows and constant store offsets)
 template <int T, bool CS = false, int FC = 0>
 __device__ __forceinline__ void emit8_trunc_i8(const double (&v)[8], int q, int count_rt,
                                                int8_t* __restrict__ out, int64_t plane,
                                                int64_t off) {
+  if constexpr (T == 7 && FC > 0) {
+    if (q >= -1000) {
+      emit8_t7<CS, FC>(v, q, out, plane, off);
+      return;
+    }
+  }
   const int count = FC > 0 ? FC : count_rt;
   constexpr int SPW = 63 / T;  // slices per window
   constexpr int WB = SPW * T;  // window bits
