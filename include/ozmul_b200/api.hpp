@@ -17,6 +17,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <functional>
 #include <optional>
 #include <span>
 #include <stdexcept>
@@ -227,6 +228,24 @@ MultiplyResult multiply(const Matrix& a, const Matrix& b, const MmaConfig& cfg,
                         const MultiplyPlan& plan);
 MultiplyResult multiply_axpby(double alpha, const Matrix& a, const Matrix& b, double beta,
                               const Matrix& c, const MmaConfig& cfg, const MultiplyPlan& plan);
+
+// The operator hook callers plug the emulated product into
+// (`GemmFn`, oracle.hpp:117; consumed by block_lu_solve, oracle.cpp:371):
+// the callable the reference's callers build by hand (main.cpp:578-582,
+// acceptance_test.cpp:278-282) -- a plan made per call for the operands'
+// inner dimension, then the GPU multiply.  The alias is the reference's own
+// type, so the two may be declared together.
+using GemmFn = std::function<Matrix(const Matrix&, const Matrix&)>;
+inline GemmFn make_gemm_fn(const MmaConfig& cfg, int slices_a, int slices_b,
+                           ScheduleKind schedule = ScheduleKind::kReduced,
+                           Accumulation strategy = Accumulation::kLevelledExact,
+                           SliceMode mode = SliceMode::kTruncate, int precision = 53) {
+  return [=](const Matrix& x, const Matrix& y) {
+    const MultiplyPlan plan = make_plan(cfg, static_cast<std::int64_t>(x.cols()), slices_a,
+                                        slices_b, schedule, strategy, mode, precision);
+    return multiply(x, y, cfg, plan).c;
+  };
+}
 
 // ============================================================ analysis
 // analysis.hpp:30-107

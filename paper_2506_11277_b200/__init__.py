@@ -36,7 +36,9 @@ __all__ = [
     "multiply_axpby", "multiply_device", "select_slices", "scaling_profile", "split_rows",
     "split_cols", "integer_gemm", "chi", "plan_levels", "spare_carries",
     "diagonal_flush_threshold", "optimal_slice_width", "max_inner_dim", "random_uniform",
-    "gen_kappa_d", "kernel_launches", "library_path", "split_i8", "pair_planes",
+    "gen_kappa_d", "kernel_launches", "library_path", "split_i8", "pair_planes", "gemm_fn",
+    "multiply_device_multi", "min_exact_slices", "exact_gemm", "forward_error",
+    "max_elementwise_error", "frobenius_norm", "normwise_gemm_error",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -524,6 +526,22 @@ def multiply_axpby(alpha: float, a, b, beta: float, c, cfg: MmaConfig, plan: Mul
                                   _dp(c), n, _dp(out), n, cfg._c(), ctypes.byref(pc),
                                   ctypes.byref(d)))
     return MultiplyResult(out, Diagnostics._from_c(d))
+
+
+def gemm_fn(cfg: MmaConfig, slices_a: int, slices_b: int,
+            schedule: ScheduleKind = ScheduleKind.REDUCED,
+            strategy: Accumulation = Accumulation.LEVELLED_EXACT,
+            mode: SliceMode = SliceMode.TRUNCATE, precision: int = 53,
+            device: Optional[int] = None):
+    """The operator hook (`GemmFn`, oracle.hpp:117, consumed by block_lu_solve,
+    oracle.cpp:371): a callable (x, y) -> x @ y that makes its plan per call
+    for the operands' inner dimension, as the reference's callers do
+    (main.cpp:578-582, acceptance_test.cpp:278-282)."""
+    def fn(x, y):
+        x = _f64(x)
+        plan = make_plan(cfg, x.shape[1], slices_a, slices_b, schedule, strategy, mode, precision)
+        return multiply(x, y, cfg, plan, device=device).c
+    return fn
 
 
 def multiply_device(m: int, n: int, k: int, a_ptr: int, lda: int, b_ptr: int, ldb: int,

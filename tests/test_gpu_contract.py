@@ -192,3 +192,33 @@ def test_device_sharded_multiply(oz, slots, peer, monkeypatch):
     s.synchronize()
     flags = [v != 0 for v in status.cpu().tolist()]
     assert flags == ([False, True] if len(slots) == 2 else [False, False, True, True])
+
+
+def test_cpp_gemm_fn_hook(tmp_path):
+    """ozmul::make_gemm_fn, the GemmFn operator hook (oracle.hpp:117) of the
+    C++ drop-in: bitwise the reference callers' hand-built lambda
+    (main.cpp:578-582), and a block LU whose Schur updates go through it
+    solves its system (tests/native/gemm_fn_test.cpp)."""
+    import os
+    import subprocess
+    from conftest import ROOT
+    lib = os.path.join(ROOT, "paper_2506_11277_b200", "lib")
+    exe = str(tmp_path / "gemm_fn_test")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "native", "gemm_fn_test.cpp"),
+                    os.path.join(lib, "libozgpu.so"), "-Wl,-rpath," + lib, "-o", exe], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.startswith("ok"), r.stdout
+
+
+def test_python_gemm_fn_hook(oz):
+    """The Python mirror of the hook: gemm_fn(cfg, sa, sb) makes its plan per
+    call from the operands' inner dimension, bitwise multiply() with that plan."""
+    rng = np.random.default_rng(17)
+    cfg = oz.MmaConfig.int8_int32()
+    fn = oz.gemm_fn(cfg, 9, 8)
+    for m, k, n in [(300, 16, 290), (129, 700, 65), (1, 1, 1)]:
+        x, y = uniform(m, k, rng), uniform(k, n, rng)
+        want = oz.multiply(x, y, cfg, oz.make_plan(cfg, k, 9, 8)).c
+        assert bits_equal(fn(x, y), want), (m, k, n)
