@@ -309,6 +309,11 @@ def bad_clocks(c) -> bool:
     return False
 
 
+# tcgen05 kind::i8 issue rate per SM: one 128x256x32 MMA (2*128*256*32 ops)
+# per 128 cycles (tools/ubench/mma_rate.cu)
+I8_OPS_PER_CLK_SM = 2 * 128 * 256 * 32 // 128
+
+
 def _peaks():
     """(int8 dense peak, its sustained twin, HBM GB/s, how) from the
     driver-measured bf16 cuBLAS rates (sm_100 int8 dense = 2x bf16 per clock)."""
@@ -572,8 +577,9 @@ def main():
                          "frac": tops / peak, "traffic": None,
                          "peak_kind": "measured: 2 x bf16 cuBLAS burst (MEASURED_PEAKS.json)",
                          "frac_sustained": tops / peak_sus, "peak_sustained": peak_sus,
-                         "kernel": "gemm_i8_pair_kernel<6> (tcgen05.mma.cta_group::2.kind::i8, "
-                                   "256x256 tiles, equal-length chunk bins, wave lockstep)",
+                         "kernel": "gemm_i8_pair_kernel (tcgen05.mma.cta_group::2.kind::i8; "
+                                   "256x512 tiles when they fill the SMs, else 256x256; "
+                                   "equal-length chunk bins, wave lockstep, split-k tail)",
                          "algorithmic": "2*chi*m*n*k int8 ops per launch (%.4g)" %
                                         (2.0 * ch * m_ * n_ * k_),
                          "launch_ms": g_ms, "peak_note": peak_how},
@@ -613,6 +619,18 @@ def main():
         "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
         "clocks": clocks,
     }
+    if clocks.get("sm_mhz"):
+        # the tensor pipe's own limit at the clock the run actually held: a
+        # power-capped long step runs well below max clock, a short unthrottled
+        # one above the cuBLAS-derived burst figure (frac > 1 there)
+        nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+        pk = I8_OPS_PER_CLK_SM * nsm * clocks["sm_mhz"] * 1e6 / 1e12
+        line["roofline"].update({
+            "peak_at_clock": pk, "frac_at_clock": tops / pk,
+            "peak_at_clock_note": "%d SMs x %d int8 ops/clk/SM (one 128x256x32 kind::i8 MMA "
+                                  "per 128 cycles per SM, tools/ubench/mma_rate.cu) x the "
+                                  "median SM clock of the timed region (%d MHz)" %
+                                  (nsm, I8_OPS_PER_CLK_SM, clocks["sm_mhz"])})
     if world > 1:
         line["exchange"] = ("A row-panel (%d x %d) broadcast along row groups, B column-panel "
                             "(%d x %d) along column groups (NCCL), inside every timed step" %
