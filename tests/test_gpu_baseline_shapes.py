@@ -183,3 +183,49 @@ def test_k32768_plane_budget_row_blocks(oz, ref, monkeypatch):
     assert bits_equal(c, c_unblocked), mismatch_report(c, c_unblocked)
     _check_blocks(oz, ref, a, b, c, plan, [(0, 16, 0, 16), (2032, 2048, 2032, 2048),
                                            (700, 716, 300, 316)], threads=3)
+
+
+def _edge_rows(rng, k):
+    """Rows that walk the production slicer's exponent edges: entries from
+    the block max down past 2^-64 and 2^-128 of it (window-1 shift directions,
+    a0 = 64 exactly), subnormals inside a normal row, block maxima around
+    2^-1000 (the t = 7 fast emit needs q >= -1000; below it the generic one
+    runs), all-subnormal and huge rows, zeros, and random-exponent rows."""
+    rows = []
+    e = np.arange(k) % 140
+    r = np.ldexp(1.0 + rng.random(k), -e)
+    r[0] = 1.5
+    rows.append(r)
+    rows.append(-r[::-1] * np.where(rng.random(k) < 0.5, 1.0, -1.0))
+    r = np.ldexp(0.5 + rng.random(k) / 2, rng.integers(-20, 1, k))
+    r[::7] = np.ldexp(1.0, -1060) * (1 + np.arange(len(r[::7])))  # subnormals in a normal row
+    rows.append(r)
+    r = np.ldexp(1.0, 64 - np.arange(k) % 66)  # exact powers: a0 = 0 .. 65 around 64
+    rows.append(r * np.where(np.arange(k) % 3 == 0, -1.0, 1.0))
+    for top in (-1001, -1002, -1003):  # q = -1000 (fast emit), -1001, -1002 (generic)
+        r = np.ldexp(1.0 + rng.random(k), top - rng.integers(0, 60, k))
+        r[1] = np.ldexp(1.5, top)
+        rows.append(r * np.where(rng.random(k) < 0.5, 1.0, -1.0))
+    rows.append(np.ldexp(1.0 + np.arange(k), -1074 + 10) * np.where(np.arange(k) % 2, 1.0, -1.0))
+    r = np.ldexp(1.0 + rng.random(k), 1020 - rng.integers(0, 200, k))
+    rows.append(r)
+    rows.append(np.zeros(k))
+    for _ in range(6):
+        rows.append(np.ldexp(rng.random(k) - 0.5, rng.integers(-80, 80, k)))
+    x = np.array(rows)
+    x[x == 0] = 0.0  # no -0 (rejected inputs)
+    return x
+
+
+@pytest.mark.parametrize("count", [1, 4, 9, 10, 12, 13, 14, 17])
+@pytest.mark.parametrize("k", [200, 201])
+def test_production_slicer_exponent_edges(oz, ref, count, k):
+    """The production int8 slicers (rows and columns; k = 200 takes the
+    vectorised kernels with a compile-time slice count, k = 201 the scalar
+    ones) bit-exact against the reference's split() on rows built to hit
+    every branch of the windowed extraction."""
+    rng = np.random.default_rng(count * 1000 + k)
+    x = _edge_rows(rng, k)
+    idx = np.arange(x.shape[0])
+    _check_slices_rows(oz, ref, x, count, idx)
+    _check_slices_cols(oz, ref, np.ascontiguousarray(x.T), count, idx)
