@@ -26,12 +26,18 @@ def main():
     ap.add_argument("--s", type=int, nargs=2, default=[12, 12])
     ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--rounds", type=int, default=3)
+    ap.add_argument("--pageable", action="store_true", help="plain numpy buffers (staged path)")
     ap.add_argument("variants", nargs="*", default=[""])
     a = ap.parse_args()
     n, k, m = a.n, a.k or a.n, a.m or a.n
-    A = torch.from_numpy(oz.random_uniform(m, k, 1, -0.5, 0.5)).pin_memory().numpy()
-    B = torch.from_numpy(oz.random_uniform(k, n, 2, -0.5, 0.5)).pin_memory().numpy()
-    C = torch.empty((m, n), dtype=torch.float64).pin_memory().numpy()
+    if a.pageable:
+        A = oz.random_uniform(m, k, 1, -0.5, 0.5)
+        B = oz.random_uniform(k, n, 2, -0.5, 0.5)
+        C = np.empty((m, n), dtype=np.float64)
+    else:
+        A = torch.from_numpy(oz.random_uniform(m, k, 1, -0.5, 0.5)).pin_memory().numpy()
+        B = torch.from_numpy(oz.random_uniform(k, n, 2, -0.5, 0.5)).pin_memory().numpy()
+        C = torch.empty((m, n), dtype=torch.float64).pin_memory().numpy()
     cfg = oz.MmaConfig.int8_int32()
     plan = oz.make_plan(cfg, k, *a.s)
     ref = None
