@@ -1542,9 +1542,12 @@ void host_multiply_locked(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const
     std::mutex stage_mu;
     std::condition_variable stage_cv;
     std::thread stager;
+    // the staging copies are memory-latency bound: two threads per core
+    // (capped at 32) measured 40.4 vs 41.5 ms at 8192^3, 53 vs 59 ms at
+    // 65536 x 2048^2 against one per core on the 16-core B200 host
     const int stage_threads = std::max(
         1, pipe_env("OZGPU_STAGE_THREADS",
-                    static_cast<int>(std::min(16u, std::max(1u, std::thread::hardware_concurrency())))));
+                    static_cast<int>(std::min(32u, 2 * std::max(1u, std::thread::hardware_concurrency())))));
     if (hs) {
       stager = std::thread([&] {
         for (size_t q = 0; q < arrivals.size() && !stop_staging.load(); ++q) {
