@@ -247,7 +247,8 @@ int ozgpu_dgemm_device(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const do
  * is ordered after `stream` (a cudaStream_t on src_device) and `stream`
  * waits for every block, so the call returns without synchronising, like
  * ozgpu_dgemm_device.  dev_status: NULL or `count` device ints on
- * src_device, one per block (0 ok, nonzero: that block saw Inf / NaN / -0).
+ * src_device, one per block (0 ok, nonzero: that block saw Inf / NaN / -0;
+ * a product too small to split runs as one block, the other slots read 0).
  * Bit-identical to ozgpu_dgemm_device. */
 int ozgpu_dgemm_device_multi(ozgpu_ctx* const* ctxs, int count, int src_device, int64_t m,
                              int64_t n, int64_t k, const double* a, int64_t lda, const double* b,

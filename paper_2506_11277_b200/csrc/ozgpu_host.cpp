@@ -2567,6 +2567,7 @@ int ozgpu_dgemm_device_multi(ozgpu_ctx* const* ctxs, int count, int src_device, 
     force_peer = fe && std::string(fe) == "1";
   });
   if (rc != OZGPU_OK) return rc;
+  const int slots = count;
   if (m < pr || n < pc) {  // every block must be non-empty: one context does it all
     count = 1;
     pr = pc = 1;
@@ -2576,6 +2577,9 @@ int ozgpu_dgemm_device_multi(ozgpu_ctx* const* ctxs, int count, int src_device, 
   rc = guarded([&] {
     cudaStream_t caller = static_cast<cudaStream_t>(stream);
     OZ_CUDA(cudaSetDevice(src_device));
+    // every slot reads 0 unless its block sees a bad input (slots past the
+    // block count when the product is too small to split stay 0)
+    if (dev_status) OZ_CUDA(cudaMemsetAsync(dev_status, 0, sizeof(int) * slots, caller));
     cudaEvent_t ready = nullptr;
     OZ_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
     std::unique_ptr<CUevent_st, decltype(&cudaEventDestroy)> ready_guard(ready, &cudaEventDestroy);

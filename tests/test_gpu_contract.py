@@ -192,6 +192,16 @@ def test_device_sharded_multiply(oz, slots, peer, monkeypatch):
     s.synchronize()
     flags = [v != 0 for v in status.cpu().tolist()]
     assert flags == ([False, True] if len(slots) == 2 else [False, False, True, True])
+    # too small to split (m < p_r): one block, every slot written
+    status.fill_(-1)
+    tiny = torch.from_numpy(uniform(1, k, rng)).to(dev)
+    ct = torch.empty(1, n, dtype=torch.float64, device=dev)
+    oz.multiply_device_multi(1, n, k, tiny.data_ptr(), k, B.data_ptr(), n + 24, ct.data_ptr(), n,
+                             cfg, plan, slots, stream=s.cuda_stream, status_ptr=status.data_ptr())
+    s.synchronize()
+    assert status.cpu().tolist() == [0] * len(slots)
+    want_t = oz.multiply(tiny.cpu().numpy(), b, cfg, plan).c
+    assert bits_equal(ct.cpu().numpy(), want_t)
 
 
 def test_cpp_gemm_fn_hook(tmp_path):
