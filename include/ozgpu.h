@@ -265,7 +265,9 @@ int ozgpu_split(ozgpu_ctx* ctx, int orientation, int64_t rows, int64_t cols, con
                 int* scales_out);
 /* The production int8 slicer (the kernels ozgpu_dgemm* launch for its
  * operands: rowmax + streaming row slicer for A, column max + transposing
- * column slicer for B in truncate mode at t <= 7; generic kernels otherwise)
+ * column slicer for B in truncate mode at t <= 7; generic kernels otherwise;
+ * for small products, (m + n) k < 8M, multiply fuses both operands into two
+ * launches that run the same row / column device code)
  * with its output as the GEMM reads it: slices_out [count][blocks][ld] int8,
  * K-major (blocks = rows for orientation 0, cols for 1; ld a multiple of 128
  * >= the block length, the tail zero-filled), scales_out per block.

@@ -753,6 +753,14 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
       slB = wb;
       qa = wqa;
       qb = wqb;
+    } else if (small_slicing_applies(m, n, k, ld, t, p.mode, da, lda)) {
+      // small operands: two launches cover both (launch latency dominates)
+      OZ_CUDA(launch_slice_small(da, lda, m, db, ldb, n, k, ld, sa, sb, wa, m * ld, wb, n * ld, wqa,
+                                 wqb, colmax, status, st, &launches));
+      slA = wa;
+      slB = wb;
+      qa = wqa;
+      qb = wqb;
     } else {
     // A's and B's slicing are independent: B's runs on a forked stream so
     // the two HBM-bound chains overlap (their tails and the short memsets

@@ -123,6 +123,18 @@ cudaError_t launch_slice_cols(const double* b, int64_t ldb, int64_t k, int64_t n
                               int width, int count, int mode, void* out, int out_is_i64,
                               int* scales, unsigned long long* colmax, int* status,
                               cudaStream_t st, int64_t* launches, int64_t plane = 0);
+// Small operands ((m + n) k < 8M entries, truncate mode, t = 7, 16-byte
+// aligned A with an even lda, kp % 128 == 0): both operands' block maxima in
+// one launch and both operands' slices in a second.  Returns false (nothing
+// launched) when the shape does not qualify.
+bool small_slicing_applies(int64_t m, int64_t n, int64_t k, int64_t kp, int width, int mode,
+                           const double* a, int64_t lda);
+cudaError_t launch_slice_small(const double* a, int64_t lda, int64_t m, const double* b,
+                               int64_t ldb, int64_t n, int64_t k, int64_t kp, int count_a,
+                               int count_b, int8_t* out_a, int64_t plane_a, int8_t* out_b,
+                               int64_t plane_b, int* scales_a, int* scales_b,
+                               unsigned long long* colmax, int* status, cudaStream_t st,
+                               int64_t* launches);
 // One persistent launch slicing A (rows) and / or B (columns) in truncate
 // mode at width <= 7 into int8, reading each operand once from DRAM (ordered
 // work queue over L2-sized panels).  a or b may be null (one operand only).

@@ -382,15 +382,15 @@ __device__ __forceinline__ void emit8_trunc_i8(const double (&v)[8], int q, int 
 // slice stores, so both kernels stream at HBM rate): rowmax_kernel computes
 // the block scales (one warp per row, 16-byte loads), slice_rows_stream_kernel
 // then slices 8 consecutive entries per thread over the whole matrix.
+// (bodies take the block index and block count, so the small-operand
+// kernel below can run them side by side in one launch)
 template <bool VEC>
-__global__ void __launch_bounds__(256) rowmax_kernel(const double* __restrict__ a, int64_t lda,
-                                                     int64_t m, int64_t k,
-                                                     int* __restrict__ scales,
-                                                     int* __restrict__ status) {
+__device__ __forceinline__ void rowmax_body(int64_t blk, int64_t nblk, const double* __restrict__ a,
+                                            int64_t lda, int64_t m, int64_t k,
+                                            int* __restrict__ scales, int* __restrict__ status) {
   const int lane = threadIdx.x & 31;
-  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-  for (int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-       row < m; row += warps) {
+  const int64_t warps = nblk * (blockDim.x >> 5);
+  for (int64_t row = blk * (blockDim.x >> 5) + (threadIdx.x >> 5); row < m; row += warps) {
     const double* ar = a + row * lda;
     unsigned long long mx = 0;
     int bad = 0;
@@ -441,14 +441,23 @@ __global__ void __launch_bounds__(256) rowmax_kernel(const double* __restrict__ 
   }
 }
 
-template <int T, bool VEC, int MINB, int FC = 0>
-__global__ void __launch_bounds__(256, MINB) slice_rows_stream_kernel(
-    const double* __restrict__ a, int64_t lda, int64_t m, int64_t k, int64_t kp, int64_t plane,
-    int count, const int* __restrict__ scales, int8_t* __restrict__ out) {
+template <bool VEC>
+__global__ void __launch_bounds__(256) rowmax_kernel(const double* __restrict__ a, int64_t lda,
+                                                     int64_t m, int64_t k,
+                                                     int* __restrict__ scales,
+                                                     int* __restrict__ status) {
+  rowmax_body<VEC>(blockIdx.x, gridDim.x, a, lda, m, k, scales, status);
+}
+
+template <int T, bool VEC, int FC>
+__device__ __forceinline__ void slice_rows_body(int64_t blk, int64_t nblk,
+                                                const double* __restrict__ a, int64_t lda,
+                                                int64_t m, int64_t k, int64_t kp, int64_t plane,
+                                                int count, const int* __restrict__ scales,
+                                                int8_t* __restrict__ out) {
   const int64_t groups = kp / 8;
   const int64_t total = m * groups;
-  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
-       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  for (int64_t idx = blk * blockDim.x + threadIdx.x; idx < total; idx += nblk * blockDim.x) {
     const int64_t row = idx / groups, g = idx - row * groups;
     const double* ar = a + row * lda;
     const int64_t j0 = g * 8;
@@ -469,19 +478,29 @@ __global__ void __launch_bounds__(256, MINB) slice_rows_stream_kernel(
   }
 }
 
+template <int T, bool VEC, int MINB, int FC = 0>
+__global__ void __launch_bounds__(256, MINB) slice_rows_stream_kernel(
+    const double* __restrict__ a, int64_t lda, int64_t m, int64_t k, int64_t kp, int64_t plane,
+    int count, const int* __restrict__ scales, int8_t* __restrict__ out) {
+  slice_rows_body<T, VEC, FC>(blockIdx.x, gridDim.x, a, lda, m, k, kp, plane, count, scales, out);
+}
+
 // 128 (k) x 32 (n) tile transpose-and-slice into K-major [l][n][kp] int8.
 // Smem holds the tile column-major in 16-byte units with an XOR swizzle so
 // both the row-wise fill and the 8-entry column reads are conflict-light.
-template <int T, int FC = 0>
-__global__ void __launch_bounds__(256) slice_cols_fast_kernel(
-    const double* __restrict__ b, int64_t ldb, int64_t k, int64_t n, int64_t kp, int64_t plane,
-    int count,
-    const unsigned long long* __restrict__ colmax, int8_t* __restrict__ out,
-    int* __restrict__ scales) {
-  constexpr int TK = 128, TN = 32, STRIDE = TK + 2;  // doubles per column (padded)
-  __shared__ __align__(16) double tile[TN * STRIDE];
-  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * TK;
-  const int64_t n0 = static_cast<int64_t>(blockIdx.y) * TN;
+constexpr int kColTileK = 128, kColTileN = 32, kColTileStride = kColTileK + 2;
+
+template <int T, int FC>
+__device__ __forceinline__ void slice_cols_tile(int64_t bx, int64_t by, double* __restrict__ tile,
+                                                const double* __restrict__ b, int64_t ldb,
+                                                int64_t k, int64_t n, int64_t kp, int64_t plane,
+                                                int count,
+                                                const unsigned long long* __restrict__ colmax,
+                                                int8_t* __restrict__ out,
+                                                int* __restrict__ scales) {
+  constexpr int TK = kColTileK, TN = kColTileN, STRIDE = kColTileStride;  // doubles per column (padded)
+  const int64_t k0 = bx * TK;
+  const int64_t n0 = by * TN;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // swizzled position of row r in column c: 16-byte unit (r >> 1) ^ ((r >> 3) & 7)
   auto pos = [](int c, int r) {
@@ -507,7 +526,7 @@ __global__ void __launch_bounds__(256) slice_cols_fast_kernel(
       *reinterpret_cast<double2*>(&tile[pos(lane, r)]) = make_double2(v[2 * i], v[2 * i + 1]);
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x < TN && n0 + threadIdx.x < n)
+  if (bx == 0 && threadIdx.x < TN && n0 + threadIdx.x < n)
     scales[n0 + threadIdx.x] = scale_from_maxbits(colmax[n0 + threadIdx.x]);
   __syncthreads();
   // item = (column, group of 8 rows); groups fastest so a warp writes 2
@@ -526,6 +545,81 @@ __global__ void __launch_bounds__(256) slice_cols_fast_kernel(
     }
     emit8_trunc_i8<T, false, FC>(v, q, count, out, plane, col * kp + kk);
   }
+}
+
+template <int T, int FC = 0>
+__global__ void __launch_bounds__(256) slice_cols_fast_kernel(
+    const double* __restrict__ b, int64_t ldb, int64_t k, int64_t n, int64_t kp, int64_t plane,
+    int count,
+    const unsigned long long* __restrict__ colmax, int8_t* __restrict__ out,
+    int* __restrict__ scales) {
+  __shared__ __align__(16) double tile[kColTileN * kColTileStride];
+  slice_cols_tile<T, FC>(blockIdx.x, blockIdx.y, tile, b, ldb, k, n, kp, plane, count, colmax, out,
+                         scales);
+}
+
+// ----------------------------------------------------------------------------
+// Small operands ((m + n) k below ~8M entries): the four slicing launches
+// (row max, column max, row slices, column slices) cost more in launch
+// latency and ramp-up than in memory time, so they run as two launches that
+// each cover both operands -- blocks [0, ga) work on A, the rest on B (the
+// column maxima of 64-row slices meet in an atomicMax).  Runtime slice count
+// (the compile-time-count kernels buy nothing at these sizes).
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) maxes_small_kernel(
+    const double* __restrict__ a, int64_t lda, int64_t m, const double* __restrict__ b,
+    int64_t ldb, int64_t n, int64_t k, int ga, int gbx, int64_t rows_per,
+    int* __restrict__ scales_a, unsigned long long* __restrict__ colmax, int* __restrict__ status) {
+  if (static_cast<int>(blockIdx.x) < ga) {
+    rowmax_body<true>(blockIdx.x, ga, a, lda, m, k, scales_a, status);
+    return;
+  }
+  // B: 32 columns x 8 row groups per block over a slice of rows_per rows;
+  // the warp reads 32 consecutive columns of one row (256 contiguous bytes)
+  __shared__ unsigned long long red[8][32];
+  const int bb = blockIdx.x - ga;
+  const int c = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t col = static_cast<int64_t>(bb % gbx) * 32 + c;
+  const int64_t r0 = static_cast<int64_t>(bb / gbx) * rows_per;
+  const int64_t r1 = r0 + rows_per < k ? r0 + rows_per : k;
+  unsigned long long mx = 0;
+  int bad = 0;
+  if (col < n) {
+#pragma unroll 4
+    for (int64_t r = r0 + g; r < r1; r += 8) {
+      const double x = __ldcs(b + r * ldb + col);
+      bad |= dirty(x);
+      const unsigned long long v = abs_bits(x);
+      mx = v > mx ? v : mx;
+    }
+  }
+  red[g][c] = mx;
+  bad = __reduce_or_sync(0xFFFFFFFFu, bad);
+  if (bad && c == 0) atomicOr(status, bad);
+  __syncthreads();
+  if (g == 0 && col < n) {
+#pragma unroll
+    for (int u = 1; u < 8; ++u) mx = red[u][c] > mx ? red[u][c] : mx;
+    if (mx) atomicMax(colmax + col, mx);
+  }
+}
+
+template <int T, int FC>
+__global__ void __launch_bounds__(256) slices_small_kernel(
+    const double* __restrict__ a, int64_t lda, int64_t m, const double* __restrict__ b,
+    int64_t ldb, int64_t n, int64_t k, int64_t kp, int count_a, int count_b, int64_t plane_a,
+    int64_t plane_b, int ga, int gbx, const int* __restrict__ scales_a,
+    const unsigned long long* __restrict__ colmax, int8_t* __restrict__ out_a,
+    int8_t* __restrict__ out_b, int* __restrict__ scales_b) {
+  __shared__ __align__(16) double tile[kColTileN * kColTileStride];
+  if (static_cast<int>(blockIdx.x) < ga) {
+    slice_rows_body<T, true, FC>(blockIdx.x, ga, a, lda, m, k, kp, plane_a, count_a, scales_a,
+                                 out_a);
+    return;
+  }
+  const int bb = blockIdx.x - ga;
+  slice_cols_tile<T, FC>(bb % gbx, bb / gbx, tile, b, ldb, k, n, kp, plane_b, count_b, colmax,
+                         out_b, scales_b);
 }
 
 // ----------------------------------------------------------------------------
@@ -1020,6 +1114,53 @@ static void launch_cols_fast_t(const double* b, int64_t ldb, int64_t k, int64_t 
   }
   slice_cols_fast_kernel<T><<<grid, 256, 0, st>>>(b, ldb, k, n, kp, plane, count, colmax, out,
                                                   scales);
+}
+
+bool small_slicing_applies(int64_t m, int64_t n, int64_t k, int64_t kp, int width, int mode,
+                           const double* a, int64_t lda) {
+  const char* env = std::getenv("OZGPU_SLICE_SMALL");
+  if (env && std::atoi(env) == 0) return false;
+  return m > 0 && n > 0 && k > 0 && mode == 0 && width == 7 && kp % 128 == 0 &&
+         (m + n) * k < (int64_t{8} << 20) && (reinterpret_cast<uintptr_t>(a) & 15) == 0 &&
+         (lda & 1) == 0;
+}
+
+cudaError_t launch_slice_small(const double* a, int64_t lda, int64_t m, const double* b,
+                               int64_t ldb, int64_t n, int64_t k, int64_t kp, int count_a,
+                               int count_b, int8_t* out_a, int64_t plane_a, int8_t* out_b,
+                               int64_t plane_b, int* scales_a, int* scales_b,
+                               unsigned long long* colmax, int* status, cudaStream_t st,
+                               int64_t* launches) {
+  cudaError_t e = cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * n, st);
+  if (e != cudaSuccess) return e;
+  const int ga = grid_for(m, 8, 148 * 16);
+  const int gb = static_cast<int>((n + 31) / 32);
+  const int64_t rows_per = 64;  // 8 rows per thread
+  const int splits = static_cast<int>((k + rows_per - 1) / rows_per);
+  maxes_small_kernel<<<ga + gb * splits, 256, 0, st>>>(a, lda, m, b, ldb, n, k, ga, gb, rows_per,
+                                                        scales_a, colmax, status);
+  const int ga2 = grid_for(m * (kp / 8), 256, 148 * 16);
+  const int gbx = static_cast<int>(kp / kColTileK);
+  // equal slice counts (the common square plans) get the compile-time-count emit
+  const int fc = (count_a == count_b && fixed_counts()) ? count_a : 0;
+  switch (fc) {
+#define OZ_FC(c)                                                                              \
+  case c:                                                                                     \
+    slices_small_kernel<7, c><<<ga2 + gbx * gb, 256, 0, st>>>(                                \
+        a, lda, m, b, ldb, n, k, kp, count_a, count_b, plane_a, plane_b, ga2, gbx, scales_a,   \
+        colmax, out_a, out_b, scales_b);                                                      \
+    break;
+    OZ_FC(1) OZ_FC(2) OZ_FC(3) OZ_FC(4) OZ_FC(5) OZ_FC(6) OZ_FC(7) OZ_FC(8) OZ_FC(9)
+    OZ_FC(10) OZ_FC(11) OZ_FC(12) OZ_FC(13) OZ_FC(14) OZ_FC(15) OZ_FC(16) OZ_FC(17)
+#undef OZ_FC
+    default:
+      slices_small_kernel<7, 0><<<ga2 + gbx * gb, 256, 0, st>>>(
+          a, lda, m, b, ldb, n, k, kp, count_a, count_b, plane_a, plane_b, ga2, gbx, scales_a,
+          colmax, out_a, out_b, scales_b);
+      break;
+  }
+  *launches += 2;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_slice_rows(const double* a, int64_t lda, int64_t m, int64_t k, int64_t kp,
