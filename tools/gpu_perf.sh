@@ -7,7 +7,9 @@ OUT=gpurun_out
 mkdir -p $OUT
 Q="--no-e2e --no-cpu-baseline --no-sweep --no-traffic --no-north-star"
 timeout 900 python bench.py > $OUT/${TAG}_bench_c2.json 2> $OUT/${TAG}_bench_c2.err; echo "c2 rc=$?"
-for c in c1 c3 c4 ns; do
+# c1 is ~50 us per multiply: enough steps that the event timing is not the noise
+timeout 600 python bench.py --config c1 --steps 300 --warmup 10 --no-sweep > $OUT/${TAG}_bench_c1.json 2> $OUT/${TAG}_bench_c1.err; echo "c1 rc=$?"
+for c in c3 c4 ns; do
   timeout 600 python bench.py --config $c --steps 5 --no-sweep > $OUT/${TAG}_bench_$c.json 2> $OUT/${TAG}_bench_$c.err; echo "$c rc=$?"
 done
 timeout 900 python bench.py --config c5 --steps 3 --warmup 3 --no-sweep > $OUT/${TAG}_bench_c5.json 2> $OUT/${TAG}_bench_c5.err; echo "c5 rc=$?"
