@@ -563,8 +563,8 @@ __global__ void __launch_bounds__(256) slice_cols_fast_kernel(
 // (row max, column max, row slices, column slices) cost more in launch
 // latency and ramp-up than in memory time, so they run as two launches that
 // each cover both operands -- blocks [0, ga) work on A, the rest on B (the
-// column maxima of 64-row slices meet in an atomicMax).  Runtime slice count
-// (the compile-time-count kernels buy nothing at these sizes).
+// column maxima of 64-row slices meet in an atomicMax).  Equal slice counts
+// use the compile-time-count emit, unequal ones the runtime count.
 // ----------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) maxes_small_kernel(
     const double* __restrict__ a, int64_t lda, int64_t m, const double* __restrict__ b,
