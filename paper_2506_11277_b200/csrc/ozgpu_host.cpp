@@ -995,7 +995,24 @@ int* run_multiply(ozgpu_ctx* ctx, int64_t m, int64_t n, int64_t k, const double*
         // at most 512 (part, chunk) plane tiles of atomic adds (32 M int32
         // adds): bins of many short chunks (k = 32768) get fewer parts
         const int nc_last = bf.size() >= 2 ? bf[bf.size() - 1] - bf[bf.size() - 2] : 1;
-        const int P = R ? std::min(clusters / R, 512 / (R * std::max(1, nc_last))) : 0;
+        // P parts per tail unit take ceil(R P / C) rounds of 1/P unit each;
+        // pick the P that minimises that (a half-full last wave, R > C / 2,
+        // gains from several rounds of short parts: R = 38 of C = 74 at
+        // 8192^3 (12,12) runs 0.6 instead of 1 unit length at P = 5).
+        // OZGPU_TAIL_MULTI=0: one round only, P = C / R.
+        const int pmax = R ? std::min(512 / (R * std::max(1, nc_last)), gp.kblocks) : 0;
+        int P = R ? std::min(clusters / R, pmax) : 0;
+        const char* tm_env = std::getenv("OZGPU_TAIL_MULTI");
+        if (R && !(tm_env && std::atoi(tm_env) == 0)) {
+          double best = P >= 2 ? 1.0 / P : 1.0;
+          for (int q = 2; q <= pmax; ++q) {
+            const double t = static_cast<double>((R * q + clusters - 1) / clusters) / q;
+            if (t < best - 1e-9) {
+              best = t;
+              P = q;
+            }
+          }
+        }
         if (tail && gp.bin_first && R && P >= 2 && pair_tiles >= R && gp.kblocks >= P &&
             U >= clusters) {
           const int G = gp.group > 0 ? gp.group : 8;
