@@ -748,37 +748,54 @@ def main():
             line["roofline"]["traffic"] = tr["bytes"]
             line["roofline"]["traffic_detail"] = tr
 
-    # north-star sub-record: 16384^3 at the estimator's slices, own roofline
+    # sub-records measured in this same run (so the driver's own bench call
+    # carries them): the north star 16384^3, configs[2] (kappa_D 4096^3) and
+    # configs[3] (65536 x 2048^2), each at the estimator's slices with its
+    # own roofline, clocks and sampled bit-exact CPU-reference blocks
+    def sub_record(key, nsteps):
+        sc = dict(CONFIGS[key])
+        a2, b2, m2, n2 = load_panels(sc)
+        a2h, b2h = a2.cpu().numpy(), b2.cpu().numpy()
+        sl2, est2 = estimate(sc, a2h, b2h)
+        p2 = oz.make_plan(mcfg, sc["k"], *sl2)
+        c2 = torch.empty((m2, n2), dtype=torch.float64, device=dev)
+        step2 = make_step(a2, b2, c2, m2, n2, sc["k"], exchange=False)
+        for _ in range(3):
+            step2(p2)
+        sampler.start()
+        ms2, _ = timed(nsteps, p2, step2)
+        clk2 = sampler.stop()
+        s2, g2, cc2 = stage_split(nsteps, p2, step2)
+        tops2, roofs2 = rooflines(m2, n2, sc["k"], sl2, g2, s2, cc2)
+        if clk2.get("sm_mhz"):
+            nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+            pk = I8_OPS_PER_CLK_SM * nsm * clk2["sm_mhz"] * 1e6 / 1e12
+            roofs2["roofline"].update({"peak_at_clock": pk, "frac_at_clock": tops2 / pk})
+        rec = {"workload": sc["name"], "slices": list(sl2), "chi": chi_of(*sl2),
+               "estimator": est2, "steps": nsteps, "ms_per_step": ms2,
+               "value": 2.0 * m2 * n2 * sc["k"] / (ms2 * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "int8_tops": tops2, "frac_of_4500_tops_spec": tops2 / 4500.0,
+               "stage_ms": {"slicing": s2, "pair_gemms": g2, "combine": cc2},
+               **roofs2, "clocks": clk2}
+        if not args.no_cpu_baseline:
+            step2(p2)
+            torch.cuda.synchronize()
+            rec["cpu_baseline"] = cpu_sample(a2h, b2h, sl2, sc["k"], m2, n2, c2)
+        del a2, b2, c2
+        return rec
+
     if world == 1 and args.config == "c2" and not args.no_north_star:
         try:
-            ns = dict(CONFIGS["ns"])
-            a2, b2, m2, n2 = load_panels(ns)
-            a2h, b2h = a2.cpu().numpy(), b2.cpu().numpy()
-            sl2, est2 = estimate(ns, a2h, b2h)
-            p2 = oz.make_plan(mcfg, ns["k"], *sl2)
-            c2 = torch.empty((m2, n2), dtype=torch.float64, device=dev)
-            step2 = make_step(a2, b2, c2, m2, n2, ns["k"], exchange=False)
-            for _ in range(3):
-                step2(p2)
-            nsteps = 3
-            sampler.start()
-            ms2, _ = timed(nsteps, p2, step2)
-            clk2 = sampler.stop()
-            s2, g2, cc2 = stage_split(nsteps, p2, step2)
-            tops2, roofs2 = rooflines(m2, n2, ns["k"], sl2, g2, s2, cc2)
-            rec = {"workload": ns["name"], "slices": list(sl2), "chi": chi_of(*sl2),
-                   "estimator": est2, "steps": nsteps, "ms_per_step": ms2,
-                   "value": 2.0 * m2 * n2 * ns["k"] / (ms2 * 1e-3) / 1e12, "unit": "TFLOP/s",
-                   "int8_tops": tops2, "frac_of_4500_tops_spec": tops2 / 4500.0,
-                   "stage_ms": {"slicing": s2, "pair_gemms": g2, "combine": cc2},
-                   **roofs2, "clocks": clk2}
-            if not args.no_cpu_baseline:
-                step2(p2)
-                torch.cuda.synchronize()
-                rec["cpu_baseline"] = cpu_sample(a2h, b2h, sl2, ns["k"], m2, n2, c2)
-            line["north_star"] = rec
+            line["north_star"] = sub_record("ns", 3)
         except Exception as e:
             line["north_star"] = {"error": repr(e)}
+        others = {}
+        for key, nsteps in (("c3", 10), ("c4", 6)):
+            try:
+                others[key] = sub_record(key, nsteps)
+            except Exception as e:
+                others[key] = {"error": repr(e)}
+        line["other_configs"] = others
 
     # weak-scaling sub-record at N > 1: every rank an 8192^3 block (configs[1])
     if world > 1 and args.config in ("c5", "t2"):
