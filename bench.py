@@ -677,6 +677,36 @@ def main():
         except Exception as e:  # context only: never fail the bench line
             line["fp64_dgemm_reference"] = {"error": repr(e)}
 
+    # accuracy beside the speed (the other half of "vs slices"): forward
+    # error of every sweep point, of the estimator's choice and of cuBLAS
+    # DGEMM against RN(AB) from oz.exact_gemm (error-free slices, bitwise the
+    # reference's GMP exact_gemm); PAPER.md:548-550 puts DGEMM-equivalent
+    # accuracy at s = 7 for uniform inputs
+    if world == 1 and cfg.get("sweep") and not args.no_sweep:
+        try:
+            exact = torch.from_numpy(oz.exact_gemm(a_h, b_h)).to(dev)
+            e_norm = torch.linalg.norm(exact)
+            tiny = torch.finfo(torch.float64).tiny
+
+            def errs(cd):
+                diff = cd - exact
+                return {"max_rel": float((diff.abs() / exact.abs().clamp_min(tiny)).max()),
+                        "frobenius_rel": float(torch.linalg.norm(diff) / e_norm)}
+
+            acc = {"reference": "RN(AB) from oz.exact_gemm", "by_slices": {}}
+            for sv in range(cfg["sweep"][0], cfg["sweep"][1] + 1):
+                step(oz.make_plan(mcfg, k, sv, sv))
+                torch.cuda.synchronize()
+                acc["by_slices"][str(sv)] = errs(c_d)
+            step(plan)
+            torch.cuda.synchronize()
+            acc["estimator_slices"] = {"slices": list(slices), **errs(c_d)}
+            acc["cublas_dgemm"] = errs(torch.matmul(a_d, b_d))
+            line["accuracy"] = acc
+            del exact
+        except Exception as e:  # context only: never fail the bench line
+            line["accuracy"] = {"error": repr(e)}
+
     # e2e through the host-pointer C-ABI call: pinned buffers (the contract),
     # and plain pageable arrays (what std::vector / numpy callers pass)
     if not args.no_e2e:
