@@ -2827,8 +2827,8 @@ int ozgpu_integer_gemm(ozgpu_ctx* ctx, int64_t m, int64_t k, int64_t n, const in
     int64_t* dy = static_cast<int64_t*>(ctx->i64b.get(sizeof(int64_t) * k * n + 8));
     int64_t* dc = c ? static_cast<int64_t*>(ctx->i64c.get(sizeof(int64_t) * m * n + 8)) : nullptr;
     int64_t* dout = static_cast<int64_t*>(ctx->i64o.get(sizeof(int64_t) * m * n + 8));
-    if (m * k) OZ_CUDA(cudaMemcpyAsync(dx, x, sizeof(int64_t) * m * k, cudaMemcpyHostToDevice, st));
-    if (k * n) OZ_CUDA(cudaMemcpyAsync(dy, y, sizeof(int64_t) * k * n, cudaMemcpyHostToDevice, st));
+    if (m * k > 0) OZ_CUDA(cudaMemcpyAsync(dx, x, sizeof(int64_t) * m * k, cudaMemcpyHostToDevice, st));
+    if (k * n > 0) OZ_CUDA(cudaMemcpyAsync(dy, y, sizeof(int64_t) * k * n, cudaMemcpyHostToDevice, st));
     if (c) OZ_CUDA(cudaMemcpyAsync(dc, c, sizeof(int64_t) * m * n, cudaMemcpyHostToDevice, st));
     // Tensor-core path when int8 holds the operands and no partial sum can
     // leave I_T nor int32; otherwise the exact per-MAC checked path.
