@@ -64,3 +64,56 @@ def test_random_multiply_matches_reference(oz, ref, i):
     if device:
         got_d[4] = want_d[4] = 0
     assert got_d == want_d, what
+
+
+@pytest.mark.parametrize("i", range(24))
+def test_random_axpby_matches_reference(oz, ref, i):
+    """multiply_axpby (scheme.cpp:363-372): D = alpha AB + beta C with the
+    reference's two roundings, over random shapes, slices and scalars."""
+    rng = np.random.default_rng(5000 + i)
+    m, n, k = (int(rng.integers(1, 200)) for _ in range(3))
+    sa, sb = int(rng.integers(1, 10)), int(rng.integers(1, 10))
+    a = random_matrix(m, k, rng, -10, 10, 0.1)
+    b = random_matrix(k, n, rng, -10, 10, 0.1)
+    c = random_matrix(m, n, rng, -10, 10, 0.1)
+    alpha, beta = (float(x) for x in rng.choice([1.0, -1.0, 0.5, 3.25, 0.0, -2.0e-3], 2))
+    cfg = oz.MmaConfig.int8_int32()
+    plan = oz.make_plan(cfg, k, sa, sb)
+    got = oz.multiply_axpby(alpha, a, b, beta, c, cfg, plan).c
+    want = ref.ref_multiply_axpby(alpha, a, b, beta, c, sa, sb)
+    assert bits_equal(got, want), ((m, n, k, sa, sb, alpha, beta), mismatch_report(got, want))
+
+
+@pytest.mark.parametrize("i", range(24))
+def test_random_split_and_estimator_match_reference(oz, ref, i):
+    """split_rows / split_cols (slicing.cpp:67-132) bit-exact at random widths,
+    counts and modes, and the estimator's kappa scan + select_slices
+    (analysis.cpp:25-68, 142-207) on the same random operands."""
+    rng = np.random.default_rng(7000 + i)
+    rows, cols = int(rng.integers(1, 120)), int(rng.integers(1, 120))
+    width = int(rng.integers(1, 8))
+    mode = int(rng.integers(0, 2)) if width >= 2 else 0
+    count = int(rng.integers(1, 14))
+    x = random_matrix(rows, cols, rng, -30, 30, 0.15)
+    for orientation in (0, 1):
+        sm = (oz.split_rows if orientation == 0 else oz.split_cols)(x, width, count,
+                                                                     oz.SliceMode(mode))
+        wsc, wsl = ref.ref_split(x, orientation, width, count, mode)
+        assert np.array_equal(sm.scale_exponents, wsc), (orientation, width, count, mode)
+        assert np.array_equal(sm.slices, wsl), (orientation, width, count, mode)
+    k = cols
+    b = random_matrix(k, int(rng.integers(1, 90)), rng, -25, 25, 0.1)
+    prof = oz.scaling_profile(x, b)
+    ka, kb, za, zb = ref.ref_scaling_profile(x, b)
+    assert (prof.kappa_a, prof.kappa_b, prof.a_has_zero_block, prof.b_has_zero_block) == \
+        (ka, kb, za, zb)
+    target = float(rng.choice([1e-8, 1e-12, 1e-15]))
+    want = ref.ref_select_slices(ka, kb, 7, 2.0 ** -53, 24, target=target)
+    if want.get("infeasible"):
+        with pytest.raises(oz.SelectionInfeasible):
+            oz.select_slices(ka, kb, 7, 2.0 ** -53, 24, oz.SelectOptions(target=target))
+        return
+    got = oz.select_slices(ka, kb, 7, 2.0 ** -53, 24, oz.SelectOptions(target=target))
+    assert (got.slices_a, got.slices_b, got.products) == \
+        (want["slices_a"], want["slices_b"], want["products"])
+    assert got.lhs == want["lhs"] and got.target == want["target"]
