@@ -812,6 +812,7 @@ def main():
             torch.cuda.synchronize()
             rec["cpu_baseline"] = cpu_sample(a2h, b2h, sl2, sc["k"], m2, n2, c2)
         del a2, b2, c2
+        torch.cuda.empty_cache()  # give the next sub-record (or the library) the memory back
         return rec
 
     if world == 1 and args.config == "c2" and not args.no_north_star:
@@ -820,7 +821,9 @@ def main():
         except Exception as e:
             line["north_star"] = {"error": repr(e)}
         others = {}
-        for key, nsteps in (("c3", 10), ("c4", 6)):
+        # configs[4] on this one GPU too: the N = 1 point of its strong-scaling
+        # series (the N > 1 lines run configs[4] sharded), ~40 s
+        for key, nsteps in (("c3", 10), ("c4", 6), ("c5", 2)):
             try:
                 others[key] = sub_record(key, nsteps)
             except Exception as e:
