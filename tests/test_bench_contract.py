@@ -93,18 +93,20 @@ def test_multi_rank_bench_path_on_one_gpu():
 @pytest.mark.gpu
 def test_headline_line_sub_records():
     """The driver's default config carries the accuracy sweep and the
-    north-star / configs[2] / configs[3] sub-records, each bit-exact on its
-    sampled CPU-reference blocks."""
+    north-star / configs[2] / configs[3] / configs[4] sub-records, each
+    bit-exact on its sampled CPU-reference blocks."""
     d = _run(["--steps", "3", "--warmup", "3", "--no-e2e", "--no-traffic"], 1500)
     acc = d["accuracy"]
     assert "error" not in acc, acc
     errs = [acc["by_slices"][str(s)]["frobenius_rel"] for s in range(3, 9)]
     assert all(x > y for x, y in zip(errs, errs[1:])), errs  # more slices, smaller error
     assert acc["estimator_slices"]["frobenius_rel"] < acc["cublas_dgemm"]["frobenius_rel"]
-    for rec in [d["north_star"], d["other_configs"]["c3"], d["other_configs"]["c4"]]:
+    for rec in [d["north_star"], d["other_configs"]["c3"], d["other_configs"]["c4"],
+                d["other_configs"]["c5"]]:
         assert "error" not in rec, rec
         assert rec["value"] > 1.0 and rec["roofline"]["achieved"] > 0
         assert rec["cpu_baseline"]["blocks_bit_exact_vs_gpu"] is True
     assert d["other_configs"]["c3"]["slices"] == [16, 17]
     assert d["other_configs"]["c4"]["slices"] == [12, 11]
     assert d["north_star"]["slices"] == [13, 12]
+    assert d["other_configs"]["c5"]["slices"] == [13, 12]
